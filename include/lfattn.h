@@ -1,0 +1,164 @@
+/*
+ * lfattn.h -- C ABI of the B200 (sm_100a) Light Forcing sparse-attention hot path.
+ *
+ * One shared library (paper_2602_04789_b200/_lib/liblfattn.so), plain C types,
+ * device pointers, explicit shapes/strides and a caller-supplied cudaStream_t.
+ * Nothing here allocates or frees caller memory; scratch comes from a caller
+ * workspace sized by lf_hsa_workspace_bytes().  Every call is stream-ordered and
+ * graph-capturable (TMA descriptors travel as __grid_constant__ kernel params).
+ *
+ * Each entry point replaces a function of the reference package chunkattn 0.1.0
+ * (/root/reference/pkg/src/chunkattn); the file:line it stands in for is given
+ * beside it.  Status codes map 1:1 onto the reference's exceptions in the Python
+ * wrapper (paper_2602_04789_b200/_lib.py).
+ */
+#ifndef LFATTN_H
+#define LFATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (lf_strerror) ------------------------------------------ */
+#define LF_OK 0
+#define LF_ERR_INVALID 1          /* ValueError: bad shape / argument          */
+#define LF_ERR_CUDA 2             /* CUDA runtime error (lf_last_error())       */
+#define LF_ERR_UNSUPPORTED 3      /* shape outside what the kernels implement   */
+#define LF_ERR_ZERO_ACTIVE_ROW 4  /* ZeroActiveRowError (attention.py:99-100)   */
+#define LF_ERR_DEGENERATE 5       /* DegenerateScheduleError (planner.py:24-25) */
+#define LF_ERR_NO_DRIVER 6        /* cuTensorMapEncodeTiled not resolvable      */
+
+/* ---- element types ------------------------------------------------------- */
+#define LF_F32 0
+#define LF_BF16 1
+
+/* A token axis cut into blocks.  `period` = tokens per independently tiled run:
+ * the whole axis for the reference's contiguous tiling (attention.py:75-87),
+ * tokens-per-frame n for the framewise ragged extension.  Block g
+ * of run t covers [t*period + j*block, min(+block, (t+1)*period, total)). */
+typedef struct {
+  int32_t total;
+  int32_t period;
+  int32_t block;
+} lf_tiling;
+
+/* Per-head row-major matrices [heads][rows][d] with arbitrary strides (in
+ * elements), so [H, L, d] and [L, H, d] layouts are both accepted. */
+typedef struct {
+  const void* ptr;
+  int32_t dtype; /* LF_F32 or LF_BF16 */
+  int32_t heads;
+  int32_t rows;
+  int32_t d;
+  int64_t row_stride;
+  int64_t head_stride;
+} lf_mat;
+
+/* Library identity. */
+int lf_version(void);
+const char* lf_strerror(int status);
+const char* lf_last_error(void);
+
+/* Block mean-pooling: out[h][g][:] = mean of the rows of block g, fp64 sums in
+ * row order, / size in fp64, rounded once to fp32.
+ * Replaces numerics.py:44-66 (mean_pool) as used by selection.py:108-111.
+ * max_blocks truncates the output (k_frame = mean_pool(k_block, bpf)[:past]). */
+int lf_pool_blocks(const lf_mat* x, lf_tiling tiling, int32_t max_blocks, float* out,
+                   int64_t out_head_stride, void* stream);
+
+/* Fused compress(): q_block, k_block and k_frame in two launches.
+ * Replaces selection.py:95-114. */
+int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling k_tiling,
+                int32_t blocks_per_frame, int32_t past_frames, float* q_block, float* k_block,
+                float* k_frame, void* stream);
+
+/* Hierarchical selection for every (head, query block), one warp each:
+ * frame scores (selection.py:117-122), top-k frames (:125-134,
+ * numerics.py:91-104), block top-budget inside the retrieved past frames
+ * (:137-175, global or per-frame mode), budget from s_i on device
+ * (selection.py:212-218 + planner.py:119-123).
+ *   s_i_dev        device double (e.g. plan.s + i-1); total budget is
+ *                  round_half_up((1-s_i)*chunk*current_blocks), chunk 1 -> 0 past.
+ *   out_blocks     [H][nqb][cap] ascending absolute past block ids
+ *   out_count      [H][nqb]
+ *   out_frames     [H][nqb][frame_cap] ascending retrieved past frames (-1 pad)
+ *   out_scores     optional [H][nqb][cap] fp64 block scores (NULL to skip)
+ *   out_fscores    optional [H][nqb][past_frames] fp64 frame scores
+ *   out_budget     optional int32[3]: total, past budget, clamped flag        */
+int lf_select(const float* q_block, const float* k_block, const float* k_frame, int32_t heads,
+              int32_t nqb, int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+              int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+              const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+              int32_t* out_count, int32_t* out_frames, double* out_scores, double* out_fscores,
+              int32_t* out_budget, void* stream);
+
+/* Chunk-Aware Growth plan on device (planner.py:126-175, _solve_clamped
+ * 178-208, alpha_schedule 56-66, s_max_for_chunk 113-116, chunk_block_budget
+ * 119-123).  Outputs (device): alpha[N], s[N], budgets[N], clamped[N],
+ * scalars[2] = {beta, achieved_flops_ratio}, status[1]. */
+int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f, int32_t n,
+                int32_t b_kv, int32_t d, int32_t first_chunk_dense, int32_t redistribute,
+                double* alpha, double* s, int32_t* budgets, int32_t* clamped, double* scalars,
+                int32_t* status, void* stream);
+
+/* Per query tile (128 rows): union of its query blocks' active key blocks as
+ * <=64-key segments {token start, length, query-block bitmask, 0}.  Segments
+ * from block lists `blocks[H][nqb][cap]` / `count[H][nqb]` over the first
+ * `list_blocks` key blocks of `k_tiling`.  Host-side replacement for the span
+ * coalescing of attention.py:159-165,249-262. */
+int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                  int32_t cap, lf_tiling q_tiling, lf_tiling k_tiling, int32_t list_blocks,
+                  int32_t seg_cap, int32_t* segs, int32_t* seg_count, void* stream);
+
+/* Block-sparse flash attention (tcgen05 + TMEM + TMA, bf16 in, fp32 accum).
+ * Query tile t of head h attends to its segments plus the dense key range
+ * [dense_lo, dense_hi) (every row active), with -inf exclusion of masked keys.
+ * Replaces attention.py:229-274 (block_sparse_attention, _stream_rows 168-188)
+ * and attention.py:212-226 (dense_attention: no segments, full dense range).
+ * out: [H][Lq][d] with out_row_stride/out_head_stride, dtype LF_F32 or LF_BF16.
+ * lse (optional, fp32 [H][Lq]) = natural-log sum-exp of scaled logits.
+ * err_flag (optional device int): bit 0 set if some row had no active key. */
+int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                 const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                 int32_t dense_lo, int32_t dense_hi, float scale, void* out, int32_t out_dtype,
+                 int64_t out_row_stride, int64_t out_head_stride, float* lse, int32_t* err_flag,
+                 void* stream);
+
+/* One full hot-path call for all heads of one layer at one denoising step of
+ * chunk i: compress -> select -> plan tiles -> sparse attention.  Replaces
+ * selection.py:196-231 (hsa_attention).  Workspace from lf_hsa_workspace_bytes. */
+typedef struct {
+  lf_mat q, k, v;           /* bf16; q rows = f*n, k/v rows = i*f*n          */
+  int32_t f, n, b_q, b_kv;  /* layout (ChunkLayout attention.py:45-96)       */
+  int32_t framewise;        /* 1: framewise ragged tiling        */
+  int32_t chunk_index;      /* 1-based                                        */
+  int32_t topk_frames;
+  int32_t per_frame_mode;
+  const double* s_i_dev;    /* device sparsity for this chunk                */
+  void* out;                /* [H][f*n][d]                                    */
+  int32_t out_dtype;
+  int64_t out_row_stride, out_head_stride;
+  float* lse;               /* optional                                       */
+  int32_t* err_flag;        /* optional                                       */
+} lf_hsa_args;
+
+size_t lf_hsa_workspace_bytes(const lf_hsa_args* a);
+/* Device pointers into the workspace (for reading selections back). */
+int lf_hsa_views(const lf_hsa_args* a, void* workspace, float** q_block, float** k_block,
+                 float** k_frame, int32_t** blocks, int32_t** count, int32_t** frames,
+                 int32_t** budget, int32_t* cap, int32_t* frame_cap);
+int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Helpers for the per-row drop-in functions. */
+/* out[r] = <A[r,:], x> in fp64 (compensated), A fp32 [rows][d].  frame_scores. */
+int lf_rowdot(const float* A, int32_t rows, int32_t d, const float* x, double* out, void* stream);
+/* Stable top-k (ties -> lower index) of fp64 scores; numerics.py:91-104. */
+int lf_topk(const double* scores, int32_t n, int32_t k, int32_t* out_idx, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LFATTN_H */

@@ -1,0 +1,506 @@
+// C ABI of the sm_100a hot path (see include/lfattn.h): argument checking,
+// TMA descriptor encoding, workspace carving and kernel launches.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "attn_sm100.cuh"
+#include "cag.cuh"
+#include "pool.cuh"
+#include "select.cuh"
+#include "tiles.cuh"
+
+using namespace lf;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return LF_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---- cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+EncodeTiledFn encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  });
+  return g_encode;
+}
+
+// 3-D map (d, rows, heads) over a bf16 lf_mat, 64-column x box_rows boxes, 128B swizzle
+int make_map(CUtensorMap* map, const lf_mat* m, int box_rows) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return fail(LF_ERR_NO_DRIVER, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)m->d, (cuuint64_t)m->rows, (cuuint64_t)m->heads};
+  cuuint64_t strides[2] = {(cuuint64_t)m->row_stride * 2, (cuuint64_t)m->head_stride * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(m->ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LF_ERR_INVALID, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return LF_OK;
+}
+
+int check_mat(const lf_mat* m, const char* name) {
+  if (!m || !m->ptr) return fail(LF_ERR_INVALID, "%s: null matrix", name);
+  if (m->heads < 1 || m->rows < 1 || m->d < 1)
+    return fail(LF_ERR_INVALID, "%s: empty shape (%d,%d,%d)", name, m->heads, m->rows, m->d);
+  if (m->dtype != LF_F32 && m->dtype != LF_BF16) return fail(LF_ERR_INVALID, "%s: dtype", name);
+  return LF_OK;
+}
+
+int check_tiling(lf_tiling t, const char* name) {
+  if (t.total < 1 || t.period < 1 || t.block < 1)
+    return fail(LF_ERR_INVALID, "%s: bad tiling (%d,%d,%d)", name, t.total, t.period, t.block);
+  return LF_OK;
+}
+
+// ---- pooling dispatch
+template <typename T>
+int launch_pool_t(const PoolArgs& a, int vec, int ns, cudaStream_t st) {
+  long long warps = a.job[0].warps + (a.njobs > 1 ? a.job[1].warps : 0);
+  if (warps == 0) return LF_OK;
+  dim3 grid((unsigned)((warps * 32 + 255) / 256));
+#define LF_POOL(V, N)                                        \
+  if (vec == V && ns == N) {                                 \
+    pool_kernel<T, V, N><<<grid, 256, 0, st>>>(a);           \
+    return check_launch("pool_kernel");                      \
+  }
+  LF_POOL(4, 1) LF_POOL(4, 2) LF_POOL(2, 1)
+  LF_POOL(1, 1) LF_POOL(1, 2) LF_POOL(1, 3) LF_POOL(1, 4) LF_POOL(1, 5) LF_POOL(1, 6)
+  LF_POOL(1, 7) LF_POOL(1, 8)
+#undef LF_POOL
+  return fail(LF_ERR_UNSUPPORTED, "pool: unsupported width d");
+}
+
+// vector width usable for a matrix (all rows aligned for VEC-element loads)
+void pool_shape(const lf_mat* m, int* vec, int* ns) {
+  const int esz = m->dtype == LF_BF16 ? 2 : 4;
+  auto ok = [&](int v) {
+    return m->d % (32 * v) == 0 && (m->row_stride * esz) % (v * esz) == 0 &&
+           (m->head_stride * esz) % (v * esz) == 0 &&
+           (reinterpret_cast<uintptr_t>(m->ptr) % (v * esz)) == 0;
+  };
+  if (ok(4) && m->d / 128 <= 2) {
+    *vec = 4;
+    *ns = m->d / 128;
+  } else if (ok(2) && m->d == 64) {
+    *vec = 2;
+    *ns = 1;
+  } else {
+    *vec = 1;
+    *ns = (m->d + 31) / 32;
+  }
+}
+
+PoolJob make_job(const lf_mat* x, lf_tiling t, int max_blocks, float* out, int64_t out_hs) {
+  PoolJob j;
+  j.x = x->ptr;
+  j.row_stride = x->row_stride;
+  j.head_stride = x->head_stride;
+  j.heads = x->heads;
+  j.d = x->d;
+  j.tiling = Tiling(t);
+  int cnt = j.tiling.count();
+  j.nblocks = max_blocks >= 0 && max_blocks < cnt ? max_blocks : cnt;
+  j.out = out;
+  j.out_head_stride = out_hs;
+  j.warps = j.heads * j.nblocks;
+  return j;
+}
+
+int launch_pool(PoolArgs& a, int dtype, int vec, int ns, cudaStream_t st) {
+  return dtype == LF_BF16 ? launch_pool_t<__nv_bfloat16>(a, vec, ns, st)
+                          : launch_pool_t<float>(a, vec, ns, st);
+}
+
+int max_qblocks_per_tile(lf_tiling qt) {
+  Tiling t(qt);
+  int worst = 0;
+  for (int q0 = 0; q0 < qt.total; q0 += kTileRows) {
+    int q1 = q0 + kTileRows < qt.total ? q0 + kTileRows : qt.total;
+    int n = t.block_of(q1 - 1) - t.block_of(q0) + 1;
+    worst = n > worst ? n : worst;
+  }
+  return worst;
+}
+
+struct HsaGeom {
+  int H, d, nqb, nkb, P, bpf, cap, frame_cap, ntiles, list_blocks, seg_cap, dense_lo, dense_hi;
+  lf_tiling qt, kt;
+};
+
+int hsa_geom(const lf_hsa_args* a, HsaGeom* g) {
+  if (a->f < 1 || a->n < 1 || a->b_q < 1 || a->b_kv < 1 || a->chunk_index < 1)
+    return fail(LF_ERR_INVALID, "bad layout");
+  if (!a->framewise && (a->n % a->b_q || a->n % a->b_kv))
+    return fail(LF_ERR_INVALID, "selection needs b_q and b_kv to divide n: n=%d, b_q=%d, b_kv=%d",
+                a->n, a->b_q, a->b_kv);
+  if (a->topk_frames < 0) return fail(LF_ERR_INVALID, "topk_frames must be >= 0");
+  g->H = a->q.heads;
+  g->d = a->q.d;
+  const int Lq = a->f * a->n, Lk = a->chunk_index * a->f * a->n;
+  if (a->q.rows != Lq) return fail(LF_ERR_INVALID, "q rows %d, expected %d", a->q.rows, Lq);
+  if (a->k.rows < Lk || a->v.rows < Lk)
+    return fail(LF_ERR_INVALID, "k/v rows %d/%d, expected >= %d", a->k.rows, a->v.rows, Lk);
+  g->qt = lf_tiling{Lq, a->n, a->b_q};
+  g->kt = lf_tiling{Lk, a->n, a->b_kv};
+  g->nqb = Tiling(g->qt).count();
+  g->nkb = Tiling(g->kt).count();
+  g->bpf = (a->n + a->b_kv - 1) / a->b_kv;
+  g->P = (a->chunk_index - 1) * a->f;
+  int kf = a->topk_frames < g->P ? a->topk_frames : g->P;
+  g->frame_cap = kf > 0 ? kf : 1;
+  g->cap = kf * g->bpf > 0 ? kf * g->bpf : 1;
+  g->ntiles = (Lq + kTileRows - 1) / kTileRows;
+  g->list_blocks = g->P * g->bpf;
+  int mq = max_qblocks_per_tile(g->qt);
+  if (mq > 32) return fail(LF_ERR_UNSUPPORTED, "b_q too small: %d query blocks per 128-row tile", mq);
+  int pieces = (a->b_kv + kSegKeys - 1) / kSegKeys;
+  long long sc = (long long)mq * (kf * g->bpf) * pieces;
+  long long all = (long long)g->list_blocks * pieces;
+  sc = sc < all ? sc : all;
+  g->seg_cap = sc > 0 ? (int)sc : 1;
+  g->dense_lo = g->P * a->n;
+  g->dense_hi = Lk;
+  return LF_OK;
+}
+
+struct HsaWs {
+  float *q_block, *k_block, *k_frame;
+  int *blocks, *count, *frames, *budget, *seg_count;
+  int4* segs;
+  size_t bytes;
+};
+
+HsaWs carve(const HsaGeom& g, void* base) {
+  HsaWs w;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + (bytes ? bytes : 16), 256);
+    return reinterpret_cast<char*>(base) + o;
+  };
+  w.q_block = reinterpret_cast<float*>(take((size_t)g.H * g.nqb * g.d * 4));
+  w.k_block = reinterpret_cast<float*>(take((size_t)g.H * g.nkb * g.d * 4));
+  w.k_frame = reinterpret_cast<float*>(take((size_t)g.H * g.P * g.d * 4));
+  w.blocks = reinterpret_cast<int*>(take((size_t)g.H * g.nqb * g.cap * 4));
+  w.count = reinterpret_cast<int*>(take((size_t)g.H * g.nqb * 4));
+  w.frames = reinterpret_cast<int*>(take((size_t)g.H * g.nqb * g.frame_cap * 4));
+  w.budget = reinterpret_cast<int*>(take(16));
+  w.segs = reinterpret_cast<int4*>(take((size_t)g.H * g.ntiles * g.seg_cap * 16));
+  w.seg_count = reinterpret_cast<int*>(take((size_t)g.H * g.ntiles * 4));
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int lf_version(void) { return 100; }
+
+const char* lf_strerror(int status) {
+  switch (status) {
+    case LF_OK: return "ok";
+    case LF_ERR_INVALID: return "invalid argument";
+    case LF_ERR_CUDA: return "CUDA error";
+    case LF_ERR_UNSUPPORTED: return "unsupported shape";
+    case LF_ERR_ZERO_ACTIVE_ROW: return "query-block row has no active key blocks";
+    case LF_ERR_DEGENERATE: return "degenerate schedule";
+    case LF_ERR_NO_DRIVER: return "CUDA driver entry point unavailable";
+  }
+  return "unknown status";
+}
+
+const char* lf_last_error(void) { return g_err; }
+
+int lf_pool_blocks(const lf_mat* x, lf_tiling tiling, int32_t max_blocks, float* out,
+                   int64_t out_head_stride, void* stream) {
+  int rc;
+  if ((rc = check_mat(x, "x")) || (rc = check_tiling(tiling, "tiling"))) return rc;
+  if (tiling.total != x->rows) return fail(LF_ERR_INVALID, "tiling total != rows");
+  if (x->d > 256) return fail(LF_ERR_UNSUPPORTED, "d > 256");
+  PoolArgs a;
+  a.njobs = 1;
+  a.job[0] = make_job(x, tiling, max_blocks, out, out_head_stride);
+  int vec, ns;
+  pool_shape(x, &vec, &ns);
+  return launch_pool(a, x->dtype, vec, ns, S(stream));
+}
+
+int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling k_tiling,
+                int32_t blocks_per_frame, int32_t past_frames, float* q_block, float* k_block,
+                float* k_frame, void* stream) {
+  int rc;
+  if ((rc = check_mat(q, "q")) || (rc = check_mat(k, "k"))) return rc;
+  if ((rc = check_tiling(q_tiling, "q_tiling")) || (rc = check_tiling(k_tiling, "k_tiling"))) return rc;
+  if (q->d != k->d || q->heads != k->heads) return fail(LF_ERR_INVALID, "q/k shape mismatch");
+  if (q->d > 256) return fail(LF_ERR_UNSUPPORTED, "d > 256");
+  const int d = q->d;
+  int vq, nq, vk, nk;
+  pool_shape(q, &vq, &nq);
+  pool_shape(k, &vk, &nk);
+  const int nqb = Tiling(q_tiling).count(), nkb = Tiling(k_tiling).count();
+  PoolArgs a;
+  a.job[0] = make_job(q, q_tiling, -1, q_block, (int64_t)nqb * d);
+  a.job[1] = make_job(k, k_tiling, -1, k_block, (int64_t)nkb * d);
+  if (q->dtype == k->dtype && vq == vk && nq == nk) {
+    a.njobs = 2;
+    if ((rc = launch_pool(a, q->dtype, vq, nq, S(stream)))) return rc;
+  } else {
+    a.njobs = 1;
+    if ((rc = launch_pool(a, q->dtype, vq, nq, S(stream)))) return rc;
+    a.job[0] = a.job[1];
+    if ((rc = launch_pool(a, k->dtype, vk, nk, S(stream)))) return rc;
+  }
+  if (past_frames > 0) {
+    // k_frame = mean_pool(k_block, bpf)[:past]  (selection.py:111-113)
+    lf_mat kb{k_block, LF_F32, k->heads, nkb, d, d, (int64_t)nkb * d};
+    PoolArgs b;
+    b.njobs = 1;
+    b.job[0] = make_job(&kb, lf_tiling{nkb, nkb, blocks_per_frame}, past_frames, k_frame,
+                        (int64_t)past_frames * d);
+    int vf, nf;
+    pool_shape(&kb, &vf, &nf);
+    if ((rc = launch_pool(b, LF_F32, vf, nf, S(stream)))) return rc;
+  }
+  return LF_OK;
+}
+
+static int select_smem_per_warp(int d, int P, int frame_cap, int max_cand) {
+  size_t b = align_up((size_t)d * 4, 16) + (size_t)P * 8 + (size_t)((frame_cap + 1) & ~1) * 4 +
+             (size_t)max_cand * 8;
+  return (int)align_up(b, 16);
+}
+
+int lf_select(const float* q_block, const float* k_block, const float* k_frame, int32_t heads,
+              int32_t nqb, int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+              int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+              const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+              int32_t* out_count, int32_t* out_frames, double* out_scores, double* out_fscores,
+              int32_t* out_budget, void* stream) {
+  if (!q_block || !k_block || !s_i_dev || !out_blocks || !out_count || !out_frames)
+    return fail(LF_ERR_INVALID, "lf_select: null pointer");
+  if (heads < 1 || nqb < 1 || d < 1 || blocks_per_frame < 1 || chunk_index < 1 || frames_per_chunk < 1)
+    return fail(LF_ERR_INVALID, "lf_select: bad sizes");
+  const int P = (chunk_index - 1) * frames_per_chunk;
+  if (P > 0 && !k_frame) return fail(LF_ERR_INVALID, "lf_select: k_frame null");
+  const int kf = topk_frames < P ? topk_frames : P;
+  if (frame_cap < (kf > 0 ? kf : 1)) return fail(LF_ERR_INVALID, "frame_cap too small");
+  if (cap < kf * blocks_per_frame) return fail(LF_ERR_INVALID, "cap too small");
+  const int max_cand = kf * blocks_per_frame;
+  const int spw = select_smem_per_warp(d, P, frame_cap, max_cand);
+  int wpc = (200 * 1024) / spw;
+  if (wpc < 1) return fail(LF_ERR_UNSUPPORTED, "selection working set too large");
+  wpc = wpc > 4 ? 4 : wpc;
+  SelArgs a{q_block, k_block, k_frame, heads, nqb, nkb, d, blocks_per_frame, chunk_index,
+            frames_per_chunk, topk_frames, per_frame_mode ? 1 : 0, s_i_dev, cap, frame_cap,
+            out_blocks, out_count, out_frames, out_scores, out_fscores, out_budget, wpc, spw,
+            max_cand};
+  const int smem = wpc * spw;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int warps = heads * nqb;
+  select_kernel<<<(warps + wpc - 1) / wpc, 32 * wpc, smem, S(stream)>>>(a);
+  return check_launch("select_kernel");
+}
+
+int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f, int32_t n,
+                int32_t b_kv, int32_t d, int32_t first_chunk_dense, int32_t redistribute,
+                double* alpha, double* s, int32_t* budgets, int32_t* clamped, double* scalars,
+                int32_t* status, void* stream) {
+  if (!(s_target >= 0.0 && s_target < 1.0 && s_base >= 0.0 && s_base <= 1.0))
+    return fail(LF_ERR_INVALID, "need 0 <= s_target < 1 and 0 <= s_base <= 1");
+  if (s_target > s_base) return fail(LF_ERR_INVALID, "s_target %g > s_base %g", s_target, s_base);
+  if (N < 1 || T < 1 || N > 1024) return fail(LF_ERR_INVALID, "N and T must be >= 1 (N <= 1024)");
+  if (f < 1 || n < 1 || b_kv < 1 || d < 1) return fail(LF_ERR_INVALID, "bad layout");
+  CagArgs a{s_target, s_base, N, T, f, n, b_kv, d, first_chunk_dense ? 1 : 0, redistribute ? 1 : 0,
+            alpha, s, budgets, clamped, scalars, status};
+  cag_kernel<<<1, 32, 0, S(stream)>>>(a);
+  return check_launch("cag_kernel");
+}
+
+int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                  int32_t cap, lf_tiling q_tiling, lf_tiling k_tiling, int32_t list_blocks,
+                  int32_t seg_cap, int32_t* segs, int32_t* seg_count, void* stream) {
+  int rc;
+  if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
+  if ((rc = check_tiling(k_tiling, "k_tiling"))) return rc;
+  if (!seg_count || !segs) return fail(LF_ERR_INVALID, "lf_plan_tiles: null output");
+  const int ntiles = (q_tiling.total + kTileRows - 1) / kTileRows;
+  if (list_blocks <= 0) {
+    cudaMemsetAsync(seg_count, 0, (size_t)heads * ntiles * 4, S(stream));
+    return check_launch("memset seg_count");
+  }
+  if (!blocks || !count) return fail(LF_ERR_INVALID, "lf_plan_tiles: null input");
+  if (max_qblocks_per_tile(q_tiling) > 32)
+    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per 128-row tile");
+  const int spw = list_blocks * 4;
+  int wpc = (200 * 1024) / spw;
+  if (wpc < 1) return fail(LF_ERR_UNSUPPORTED, "too many key blocks (%d)", list_blocks);
+  wpc = wpc > 4 ? 4 : wpc;
+  PlanArgs a{blocks, count, heads, nqb, cap, Tiling(q_tiling), Tiling(k_tiling), list_blocks,
+             ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc};
+  const int smem = wpc * spw;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(plan_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int warps = heads * ntiles;
+  plan_tiles_kernel<<<(warps + wpc - 1) / wpc, 32 * wpc, smem, S(stream)>>>(a);
+  return check_launch("plan_tiles_kernel");
+}
+
+int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                 const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                 int32_t dense_lo, int32_t dense_hi, float scale, void* out, int32_t out_dtype,
+                 int64_t out_row_stride, int64_t out_head_stride, float* lse, int32_t* err_flag,
+                 void* stream) {
+  int rc;
+  if ((rc = check_mat(q, "q")) || (rc = check_mat(k, "k")) || (rc = check_mat(v, "v"))) return rc;
+  if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
+  if (q->dtype != LF_BF16 || k->dtype != LF_BF16 || v->dtype != LF_BF16)
+    return fail(LF_ERR_UNSUPPORTED, "attention operands must be bf16");
+  if (q->d != k->d || k->d != v->d) return fail(LF_ERR_INVALID, "head dims differ");
+  if (q->d != 64 && q->d != 128) return fail(LF_ERR_UNSUPPORTED, "head dim %d (64 or 128)", q->d);
+  if (q->heads != k->heads || k->heads != v->heads) return fail(LF_ERR_INVALID, "heads differ");
+  if (k->rows != v->rows) return fail(LF_ERR_INVALID, "k rows != v rows");
+  if (q_tiling.total != q->rows) return fail(LF_ERR_INVALID, "q tiling total != q rows");
+  for (const lf_mat* m : {q, k, v})
+    if ((m->row_stride * 2) % 16 || (m->head_stride * 2) % 16 ||
+        reinterpret_cast<uintptr_t>(m->ptr) % 16)
+      return fail(LF_ERR_INVALID, "TMA needs 16-byte aligned rows");
+  if (dense_lo < 0 || dense_hi > k->rows) return fail(LF_ERR_INVALID, "dense range outside keys");
+  if (max_qblocks_per_tile(q_tiling) > 32)
+    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per 128-row tile");
+  if (!out) return fail(LF_ERR_INVALID, "null out");
+  AttnParams p;
+  memset(&p, 0, sizeof(p));
+  if ((rc = make_map(&p.tq, q, 128)) || (rc = make_map(&p.tk, k, 64)) || (rc = make_map(&p.tv, v, 64)))
+    return rc;
+  p.qt = Tiling(q_tiling);
+  p.Lq = q->rows;
+  p.n_qtiles = (q->rows + 127) / 128;
+  p.segs = reinterpret_cast<const int4*>(segs);
+  p.seg_count = seg_count;
+  p.seg_cap = seg_cap;
+  p.dense_lo = dense_lo;
+  p.dense_hi = dense_hi;
+  p.scale = scale;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  p.out_dtype = out_dtype;
+  p.out_row_stride = out_row_stride;
+  p.out_head_stride = out_head_stride;
+  p.lse = lse;
+  p.err = err_flag;
+  dim3 grid(p.n_qtiles, q->heads);
+  if (q->d == 128) {
+    cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         AttnCfg<128>::SMEM);
+    attn_fwd_kernel<128><<<grid, 192, AttnCfg<128>::SMEM, S(stream)>>>(p);
+  } else {
+    cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         AttnCfg<64>::SMEM);
+    attn_fwd_kernel<64><<<grid, 192, AttnCfg<64>::SMEM, S(stream)>>>(p);
+  }
+  return check_launch("attn_fwd_kernel");
+}
+
+size_t lf_hsa_workspace_bytes(const lf_hsa_args* a) {
+  HsaGeom g;
+  if (hsa_geom(a, &g)) return 0;
+  return carve(g, nullptr).bytes;
+}
+
+int lf_hsa_views(const lf_hsa_args* a, void* workspace, float** q_block, float** k_block,
+                 float** k_frame, int32_t** blocks, int32_t** count, int32_t** frames,
+                 int32_t** budget, int32_t* cap, int32_t* frame_cap) {
+  HsaGeom g;
+  int rc;
+  if ((rc = hsa_geom(a, &g))) return rc;
+  HsaWs w = carve(g, workspace);
+  if (q_block) *q_block = w.q_block;
+  if (k_block) *k_block = w.k_block;
+  if (k_frame) *k_frame = w.k_frame;
+  if (blocks) *blocks = w.blocks;
+  if (count) *count = w.count;
+  if (frames) *frames = w.frames;
+  if (budget) *budget = w.budget;
+  if (cap) *cap = g.cap;
+  if (frame_cap) *frame_cap = g.frame_cap;
+  return LF_OK;
+}
+
+int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes, void* stream) {
+  HsaGeom g;
+  int rc;
+  if (!a) return fail(LF_ERR_INVALID, "null args");
+  if ((rc = hsa_geom(a, &g))) return rc;
+  HsaWs w = carve(g, workspace);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(LF_ERR_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
+  lf_mat kview = a->k;
+  kview.rows = a->chunk_index * a->f * a->n;
+  if ((rc = lf_compress(&a->q, &kview, g.qt, g.kt, g.bpf, g.P, w.q_block, w.k_block, w.k_frame,
+                        stream)))
+    return rc;
+  if ((rc = lf_select(w.q_block, w.k_block, w.k_frame, g.H, g.nqb, g.nkb, g.d, g.bpf,
+                      a->chunk_index, a->f, a->topk_frames, a->per_frame_mode, a->s_i_dev, g.cap,
+                      g.frame_cap, w.blocks, w.count, w.frames, nullptr, nullptr, w.budget, stream)))
+    return rc;
+  if ((rc = lf_plan_tiles(w.blocks, w.count, g.H, g.nqb, g.cap, g.qt, g.kt, g.list_blocks,
+                          g.seg_cap, reinterpret_cast<int32_t*>(w.segs), w.seg_count, stream)))
+    return rc;
+  lf_mat kk = a->k, vv = a->v;
+  kk.rows = vv.rows = a->chunk_index * a->f * a->n;
+  return lf_attention(&a->q, &kk, &vv, g.qt, reinterpret_cast<const int32_t*>(w.segs), w.seg_count,
+                      g.seg_cap, g.dense_lo, g.dense_hi, 1.0f / sqrtf((float)g.d), a->out,
+                      a->out_dtype, a->out_row_stride, a->out_head_stride, a->lse, a->err_flag,
+                      stream);
+}
+
+int lf_rowdot(const float* A, int32_t rows, int32_t d, const float* x, double* out, void* stream) {
+  if (!A || !x || !out || rows < 0 || d < 1) return fail(LF_ERR_INVALID, "lf_rowdot: bad args");
+  if (rows == 0) return LF_OK;
+  rowdot_kernel<<<(rows + 127) / 128, 128, d * 4, S(stream)>>>(A, rows, d, x, out);
+  return check_launch("rowdot_kernel");
+}
+
+int lf_topk(const double* scores, int32_t n, int32_t k, int32_t* out_idx, void* stream) {
+  if (k < 0) return fail(LF_ERR_INVALID, "k must be >= 0, got %d", k);
+  if (n <= 0 || k == 0) return LF_OK;
+  if (!scores || !out_idx) return fail(LF_ERR_INVALID, "lf_topk: null");
+  topk_kernel<<<1, 256, 0, S(stream)>>>(scores, n, k < n ? k : n, out_idx);
+  return check_launch("topk_kernel");
+}
+
+}  // extern "C"

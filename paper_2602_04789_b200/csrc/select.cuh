@@ -1,0 +1,188 @@
+// K2: hierarchical selection, one warp per (head, query block).
+//
+// Restates selection.py:117-175 + numerics.py:91-104 on device:
+//   frame scores  p_t = <k_frame[t], q_block[r]>        (selection.py:117-122)
+//   frames        = top-k(p) by (-score, index)  U current chunk     (:125-134)
+//   candidates    = blocks of the retrieved past frames, ascending   (:157)
+//   block scores  o_c = <k_block[c], q_block[r]>                     (:158)
+//   global mode   : top-`budget` by (-score, index), output ascending(:160-162)
+//   per-frame mode: ceil(budget/#frames) per frame, frame-ordered
+//                   concatenation truncated to `budget`              (:163-169)
+// Scores are fp64 dot products of fp32 summaries; products are exact in fp64
+// and the sum is compensated (TwoSum), so ties between equal rows are exact
+// and near-ties resolve on the (almost always) correctly rounded value.
+// The budget is computed on device from s_i exactly like chunk_block_budget
+// (planner.py:119-123) with the selection.py:212-218 clamp.
+#pragma once
+#include "common.cuh"
+
+namespace lf {
+
+struct SelArgs {
+  const float* q_block;
+  const float* k_block;
+  const float* k_frame;
+  int heads, nqb, nkb, d, bpf, chunk, f, topk, per_frame;
+  const double* s_i;
+  int cap, frame_cap;
+  int* out_blocks;
+  int* out_count;
+  int* out_frames;
+  double* out_scores;
+  double* out_fscores;
+  int* out_budget;
+  int warps_per_cta;
+  int smem_per_warp;  // bytes
+  int max_cand;
+};
+
+__device__ __forceinline__ double dot_f32_dd(const float* __restrict__ row, const float* qv, int d) {
+  DD acc{0.0, 0.0};
+  if ((d & 3) == 0 && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+    for (int c = 0; c < d; c += 4) {
+      float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
+      dd_add(acc, (double)a.x * (double)qv[c]);
+      dd_add(acc, (double)a.y * (double)qv[c + 1]);
+      dd_add(acc, (double)a.z * (double)qv[c + 2]);
+      dd_add(acc, (double)a.w * (double)qv[c + 3]);
+    }
+  } else {
+    for (int c = 0; c < d; ++c) dd_add(acc, (double)__ldg(row + c) * (double)qv[c]);
+  }
+  return dd_value(acc);
+}
+
+// rank of element i among n scores under (-score, index) order
+__device__ __forceinline__ int stable_rank(const double* sc, int lo, int n, int i) {
+  const double si = sc[i];
+  int rank = 0;
+  for (int u = lo; u < lo + n; ++u) {
+    double su = sc[u];
+    rank += (su > si) || (su == si && u < i);
+  }
+  return rank;
+}
+
+__global__ void __launch_bounds__(128) select_kernel(SelArgs a) {
+  extern __shared__ __align__(16) unsigned char sel_smem[];
+  const int lane = threadIdx.x & 31;
+  const int wl = threadIdx.x >> 5;
+  const int w = blockIdx.x * a.warps_per_cta + wl;
+  if (w >= a.heads * a.nqb) return;
+  const int h = w / a.nqb, r = w - h * a.nqb;
+
+  unsigned char* base = sel_smem + (size_t)wl * a.smem_per_warp;
+  float* qv = reinterpret_cast<float*>(base);
+  const int P = (a.chunk - 1) * a.f;
+  double* fsc = reinterpret_cast<double*>(base + ((a.d * 4 + 15) & ~15));
+  int* fsel = reinterpret_cast<int*>(fsc + P);
+  double* csc = reinterpret_cast<double*>(fsel + ((a.frame_cap + 1) & ~1));
+
+  const float* qrow = a.q_block + ((size_t)h * a.nqb + r) * a.d;
+  for (int c = lane; c < a.d; c += 32) qv[c] = qrow[c];
+
+  // budget (selection.py:212-218, planner.py:119-123)
+  const int current = a.f * a.bpf;
+  int total = current;
+  if (a.chunk > 1) {
+    double s = *a.s_i;
+    total = (int)floor((1.0 - s) * (double)(a.chunk * current) + 0.5);
+  }
+  const int past_budget = total > current ? total - current : 0;
+  if (a.out_budget && w == 0 && lane == 0) {
+    a.out_budget[0] = total;
+    a.out_budget[1] = past_budget;
+    a.out_budget[2] = total < current;
+  }
+  __syncwarp();
+
+  // frame scores
+  const float* kf = a.k_frame + (size_t)h * P * a.d;
+  for (int t = lane; t < P; t += 32) fsc[t] = dot_f32_dd(kf + (size_t)t * a.d, qv, a.d);
+  __syncwarp();
+  if (a.out_fscores) {
+    double* o = a.out_fscores + ((size_t)h * a.nqb + r) * P;
+    for (int t = lane; t < P; t += 32) o[t] = fsc[t];
+  }
+
+  // top-k frames, emitted in ascending frame order
+  const int kf_n = a.topk < P ? a.topk : P;
+  int nsel = 0;
+  for (int b0 = 0; b0 < P; b0 += 32) {
+    int t = b0 + lane;
+    bool take = false;
+    if (t < P && kf_n > 0) take = (kf_n >= P) || stable_rank(fsc, 0, P, t) < kf_n;
+    unsigned m = __ballot_sync(0xffffffffu, take);
+    if (take) fsel[nsel + __popc(m & ((1u << lane) - 1))] = t;
+    nsel += __popc(m);
+  }
+  __syncwarp();
+  int* of = a.out_frames + ((size_t)h * a.nqb + r) * a.frame_cap;
+  for (int e = lane; e < a.frame_cap; e += 32) of[e] = e < nsel ? fsel[e] : -1;
+
+  int* ob = a.out_blocks + ((size_t)h * a.nqb + r) * a.cap;
+  double* os = a.out_scores ? a.out_scores + ((size_t)h * a.nqb + r) * a.cap : nullptr;
+  const int bpf = a.bpf;
+  const int C = nsel * bpf;
+  if (C == 0 || past_budget == 0) {
+    if (lane == 0) a.out_count[w] = 0;
+    return;
+  }
+
+  // candidate scores, ascending (frame, block)
+  const float* kb = a.k_block + (size_t)h * a.nkb * a.d;
+  for (int c = lane; c < C; c += 32) {
+    int t = fsel[c / bpf];
+    int blk = t * bpf + (c - (c / bpf) * bpf);
+    csc[c] = dot_f32_dd(kb + (size_t)blk * a.d, qv, a.d);
+  }
+  __syncwarp();
+
+  const int budget = past_budget;
+  const int per = (budget + nsel - 1) / nsel;
+  const int take_pf = per < bpf ? per : bpf;
+  int cnt = 0;
+  for (int b0 = 0; b0 < C; b0 += 32) {
+    int c = b0 + lane;
+    bool chosen = false;
+    if (c < C) {
+      if (!a.per_frame) {
+        chosen = budget >= C || stable_rank(csc, 0, C, c) < budget;
+      } else {
+        int fi = c / bpf;
+        int lr = stable_rank(csc, fi * bpf, bpf, c);
+        chosen = lr < per && fi * take_pf + lr < budget;
+      }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, chosen);
+    if (chosen) {
+      int pos = cnt + __popc(m & ((1u << lane) - 1));
+      if (pos < a.cap) {
+        int fi = c / bpf;
+        ob[pos] = fsel[fi] * bpf + (c - fi * bpf);
+        if (os) os[pos] = csc[c];
+      }
+    }
+    cnt += __popc(m);
+  }
+  if (lane == 0) a.out_count[w] = cnt < a.cap ? cnt : a.cap;
+}
+
+// frame_scores helper: out[r] = <A[r], x>
+__global__ void rowdot_kernel(const float* A, int rows, int d, const float* x, double* out) {
+  extern __shared__ float xs[];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) xs[c] = x[c];
+  __syncthreads();
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) out[r] = dot_f32_dd(A + (size_t)r * d, xs, d);
+}
+
+// stable top-k: out_idx[rank] = i for rank < k (one CTA)
+__global__ void topk_kernel(const double* sc, int n, int k, int* out_idx) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int rk = stable_rank(sc, 0, n, i);
+    if (rk < k) out_idx[rk] = i;
+  }
+}
+
+}  // namespace lf

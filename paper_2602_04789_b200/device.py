@@ -1,0 +1,221 @@
+"""Typed torch wrappers over the C ABI: one function per entry point.
+
+Everything here takes/returns CUDA tensors and enqueues work on the current
+stream; nothing synchronises.  The reference-compatible API (selection.py,
+attention.py, planner.py, numerics.py in this package) is built on these.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+SEG_KEYS = 64
+TILE_ROWS = 128
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass(frozen=True)
+class TilingSpec:
+    """A token axis cut into blocks; period = n (framewise) or total (contiguous)."""
+
+    total: int
+    period: int
+    block: int
+
+    @property
+    def per_period(self) -> int:
+        return -(-self.period // self.block)
+
+    @property
+    def count(self) -> int:
+        full, rem = divmod(self.total, self.period)
+        return full * self.per_period + -(-rem // self.block)
+
+    def block_of(self, row: int) -> int:
+        t = row // self.period
+        return t * self.per_period + (row - t * self.period) // self.block
+
+    def bounds(self):
+        """[count, 2] int64 tensor of (start, end) for every block (host)."""
+        import numpy as np
+        g = np.arange(self.count, dtype=np.int64)
+        t, j = np.divmod(g, self.per_period)
+        s = t * self.period + j * self.block
+        e = np.minimum(np.minimum(s + self.block, t * self.period + self.period), self.total)
+        return np.stack([s, e], axis=1)
+
+    def max_blocks_per_tile(self) -> int:
+        worst = 0
+        for q0 in range(0, self.total, TILE_ROWS):
+            q1 = min(q0 + TILE_ROWS, self.total)
+            worst = max(worst, self.block_of(q1 - 1) - self.block_of(q0) + 1)
+        return worst
+
+    def abi(self) -> L.LfTiling:
+        return L.tiling(self.total, self.period, self.block)
+
+
+def pool_blocks(x: torch.Tensor, spec: TilingSpec, max_blocks: int = -1) -> torch.Tensor:
+    """Block means of x [H, L, d] (bf16 or fp32) -> fp32 [H, nblocks, d]."""
+    lib = L.lib()
+    x3 = x if x.dim() == 3 else x.unsqueeze(0)
+    nb = spec.count if max_blocks < 0 else min(max_blocks, spec.count)
+    out = torch.empty((x3.shape[0], nb, x3.shape[2]), device=x.device, dtype=torch.float32)
+    m = L.mat(x3)
+    L.check(lib.lf_pool_blocks(ctypes.byref(m), spec.abi(), int(max_blocks), out.data_ptr(),
+                               nb * x3.shape[2], L.stream_ptr()))
+    return out if x.dim() == 3 else out[0]
+
+
+def compress(q: torch.Tensor, k: torch.Tensor, qt: TilingSpec, kt: TilingSpec, bpf: int,
+             past_frames: int):
+    """q_block, k_block, k_frame for [H, L, d] inputs (selection.py:95-114)."""
+    lib = L.lib()
+    H, d = q.shape[0], q.shape[2]
+    q_block = torch.empty((H, qt.count, d), device=q.device, dtype=torch.float32)
+    k_block = torch.empty((H, kt.count, d), device=q.device, dtype=torch.float32)
+    k_frame = torch.empty((H, max(past_frames, 0), d), device=q.device, dtype=torch.float32)
+    mq, mk = L.mat(q), L.mat(k)
+    L.check(lib.lf_compress(ctypes.byref(mq), ctypes.byref(mk), qt.abi(), kt.abi(), int(bpf),
+                            int(past_frames), q_block.data_ptr(), k_block.data_ptr(),
+                            k_frame.data_ptr() if past_frames > 0 else None, L.stream_ptr()))
+    return q_block, k_block, k_frame
+
+
+@dataclass
+class Selections:
+    blocks: torch.Tensor     # [H, nqb, cap] int32 ascending absolute past block ids
+    count: torch.Tensor      # [H, nqb] int32
+    frames: torch.Tensor     # [H, nqb, frame_cap] int32 (-1 padded)
+    budget: torch.Tensor     # [3] int32: total, past budget, clamped
+    scores: torch.Tensor | None = None
+    fscores: torch.Tensor | None = None
+
+
+def select(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: int, per_frame: bool,
+           s_i, want_scores: bool = False) -> Selections:
+    """Frame top-k + block top-budget for every (head, query block)."""
+    lib = L.lib()
+    H, nqb, d = q_block.shape
+    nkb = k_block.shape[1]
+    P = (chunk - 1) * f
+    kf = min(topk, P)
+    cap = max(1, kf * bpf)
+    frame_cap = max(1, kf)
+    dev = q_block.device
+    if not torch.is_tensor(s_i):
+        s_i = torch.tensor([float(s_i)], dtype=torch.float64, device=dev)
+    blocks = torch.empty((H, nqb, cap), dtype=torch.int32, device=dev)
+    count = torch.empty((H, nqb), dtype=torch.int32, device=dev)
+    frames = torch.empty((H, nqb, frame_cap), dtype=torch.int32, device=dev)
+    budget = torch.zeros(4, dtype=torch.int32, device=dev)
+    scores = torch.empty((H, nqb, cap), dtype=torch.float64, device=dev) if want_scores else None
+    fscores = torch.empty((H, nqb, max(P, 1)), dtype=torch.float64, device=dev) if want_scores else None
+    L.check(lib.lf_select(q_block.data_ptr(), k_block.data_ptr(),
+                          k_frame.data_ptr() if P > 0 else None, H, nqb, nkb, d, int(bpf),
+                          int(chunk), int(f), int(topk), 1 if per_frame else 0, s_i.data_ptr(),
+                          cap, frame_cap, blocks.data_ptr(), count.data_ptr(), frames.data_ptr(),
+                          L.ptr(scores), L.ptr(fscores), budget.data_ptr(), L.stream_ptr()))
+    return Selections(blocks, count, frames, budget, scores, fscores)
+
+
+@dataclass
+class CagPlan:
+    alpha: torch.Tensor
+    s: torch.Tensor
+    budgets: torch.Tensor
+    clamped: torch.Tensor
+    scalars: torch.Tensor   # beta, achieved
+    status: torch.Tensor
+
+
+def cag_plan(s_target, s_base, N, T, f, n, b_kv, d, first_chunk_dense=True,
+             redistribute=False) -> CagPlan:
+    lib = L.lib()
+    dev = _dev()
+    p = CagPlan(torch.empty(N, dtype=torch.float64, device=dev),
+                torch.empty(N, dtype=torch.float64, device=dev),
+                torch.empty(N, dtype=torch.int32, device=dev),
+                torch.empty(N, dtype=torch.int32, device=dev),
+                torch.empty(2, dtype=torch.float64, device=dev),
+                torch.zeros(1, dtype=torch.int32, device=dev))
+    L.check(lib.lf_cag_plan(float(s_target), float(s_base), int(N), int(T), int(f), int(n),
+                            int(b_kv), int(d), int(bool(first_chunk_dense)), int(bool(redistribute)),
+                            p.alpha.data_ptr(), p.s.data_ptr(), p.budgets.data_ptr(),
+                            p.clamped.data_ptr(), p.scalars.data_ptr(), p.status.data_ptr(),
+                            L.stream_ptr()))
+    return p
+
+
+@dataclass
+class TilePlan:
+    segs: torch.Tensor       # [H, ntiles, seg_cap, 4] int32
+    seg_count: torch.Tensor  # [H, ntiles] int32
+    seg_cap: int
+
+
+def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
+               seg_cap: int | None = None) -> TilePlan:
+    lib = L.lib()
+    H, nqb, cap = blocks.shape
+    ntiles = -(-qt.total // TILE_ROWS)
+    pieces = -(-kt.block // SEG_KEYS)
+    if seg_cap is None:
+        seg_cap = max(1, min(qt.max_blocks_per_tile() * cap * pieces, max(list_blocks, 0) * pieces))
+    dev = blocks.device
+    segs = torch.empty((H, ntiles, seg_cap, 4), dtype=torch.int32, device=dev)
+    seg_count = torch.empty((H, ntiles), dtype=torch.int32, device=dev)
+    L.check(lib.lf_plan_tiles(blocks.data_ptr(), count.data_ptr(), H, nqb, cap, qt.abi(), kt.abi(),
+                              int(list_blocks), int(seg_cap), segs.data_ptr(), seg_count.data_ptr(),
+                              L.stream_ptr()))
+    return TilePlan(segs, seg_count, seg_cap)
+
+
+def attention(q, k, v, qt: TilingSpec, tiles: TilePlan | None, dense_lo: int, dense_hi: int,
+              out: torch.Tensor | None = None, out_dtype=torch.float32, scale: float | None = None,
+              lse: torch.Tensor | None = None, err: torch.Tensor | None = None) -> torch.Tensor:
+    """Block-sparse flash attention over bf16 [H, L, d] (d in {64, 128})."""
+    lib = L.lib()
+    H, Lq, d = q.shape
+    if out is None:
+        out = torch.empty((H, Lq, d), dtype=out_dtype, device=q.device)
+    odt = L.LF_F32 if out.dtype == torch.float32 else L.LF_BF16
+    mq, mk, mv = L.mat(q), L.mat(k), L.mat(v)
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    L.check(lib.lf_attention(ctypes.byref(mq), ctypes.byref(mk), ctypes.byref(mv), qt.abi(),
+                             tiles.segs.data_ptr() if tiles else None,
+                             tiles.seg_count.data_ptr() if tiles else None,
+                             tiles.seg_cap if tiles else 0, int(dense_lo), int(dense_hi),
+                             float(scale), out.data_ptr(), odt, out.stride(1), out.stride(0),
+                             L.ptr(lse), L.ptr(err), L.stream_ptr()))
+    return out
+
+
+def rowdot(A: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    lib = L.lib()
+    A = A.contiguous().float()
+    x = x.contiguous().float()
+    out = torch.empty(A.shape[0], dtype=torch.float64, device=A.device)
+    L.check(lib.lf_rowdot(A.data_ptr(), A.shape[0], A.shape[1], x.data_ptr(), out.data_ptr(),
+                          L.stream_ptr()))
+    return out
+
+
+def topk(scores: torch.Tensor, k: int) -> torch.Tensor:
+    lib = L.lib()
+    scores = scores.contiguous().double()
+    n = scores.shape[0]
+    kk = max(0, min(k, n))
+    out = torch.empty(max(kk, 1), dtype=torch.int32, device=scores.device)
+    L.check(lib.lf_topk(scores.data_ptr(), n, int(k), out.data_ptr(), L.stream_ptr()))
+    return out[:kk]
