@@ -1,0 +1,456 @@
+#!/usr/bin/env python
+"""Benchmark of the Light Forcing sparse-attention hot path on B200.
+
+One *step* = one chunk of one layer: the T = 4 denoising-step hot-path calls
+(compress -> hierarchical selection -> tile plan -> tcgen05 block-sparse
+attention, all heads) of chunk i, each on its own synthetic Q/K/V (bf16,
+seeded N(0,1), K/V over the whole i-chunk context).  The CAG plan is solved on
+device and s_i is read from device memory by the selection kernel.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
+
+Multi-GPU (torchrun, one rank per GPU): heads are sharded when H % N == 0 and
+the per-head outputs are all-gathered over NCCL (strong scaling); otherwise
+every rank runs an independent video (replicas, weak scaling, no collective).
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+METRIC = "sparse-attn ms/chunk & effective TFLOPS (1.3B 480p) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "effective TFLOP/s"
+
+CONFIGS = {
+    # BASELINE.json configs[1]: Self-Forcing 1.3B 480p, chunk 7 of a 7-chunk rollout, CAG plan
+    "c2": dict(heads=12, d=128, n=1560, f=3, N=7, chunk=7, plan=(0.9, 0.98), s=None, topk=6,
+               mode="global", T=4),
+    # configs[2]: long rollout, chunk 14 of 21 (42 frames of KV), CAG plan -> past blocks selected
+    "c3": dict(heads=12, d=128, n=1560, f=3, N=21, chunk=14, plan=(0.9, 0.98), s=None, topk=6,
+               mode="global", T=4),
+    # configs[3]: Wan-14B attention shape (40 heads)
+    "c4": dict(heads=40, d=128, n=1560, f=3, N=7, chunk=7, plan=(0.9, 0.98), s=None, topk=6,
+               mode="global", T=4),
+    # configs[4] sweep points: fixed sparsity s at chunk 7 (0.0 = dense through the same kernel)
+    "c5_s50": dict(heads=12, d=128, n=1560, f=3, N=7, chunk=7, plan=None, s=0.5, topk=6,
+                   mode="global", T=4),
+    "c5_s70": dict(heads=12, d=128, n=1560, f=3, N=7, chunk=7, plan=None, s=0.7, topk=6,
+                   mode="global", T=4),
+    "c5_s85": dict(heads=12, d=128, n=1560, f=3, N=7, chunk=7, plan=None, s=0.85, topk=6,
+                   mode="global", T=4),
+    "c5_dense": dict(heads=12, d=128, n=1560, f=3, N=7, chunk=7, plan=None, s=0.0, topk=18,
+                     mode="global", T=4),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-launch", action="store_true",
+                    help="run 2 eager steps only (for ncu launch lists)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- helpers
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms in the background."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "200", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except OSError:
+            return self
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_desc():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def make_layout(lf, c):
+    return lf.ChunkLayout(f=c["f"], n=c["n"], b_q=64, b_kv=64, d=c["d"], N=c["N"])
+
+
+def host_s(lf, c, lay):
+    """s_i for the config (host value, for the CPU legs)."""
+    if c["plan"] is None:
+        return float(c["s"])
+    from oracle import lf_oracle as O
+    p = O.allocate(c["plan"][0], c["plan"][1], c["N"], c["T"], c["f"], c["n"], 64, c["d"])
+    return p.s[c["chunk"] - 1]
+
+
+# ---------------------------------------------------------------------------- CPU legs
+
+
+def oracle_sample(c, s_i, seed, threads):
+    """Time the CPU oracle (framewise port of chunkattn.hsa_attention) on one head."""
+    import numpy as np
+    from oracle import lf_oracle as O
+    i, f, n, d = c["chunk"], c["f"], c["n"], c["d"]
+    q, k, v = O.synthetic_qkv(seed, f * n, i * f * n, d)
+    t0 = time.perf_counter()
+    out, sel, _ = O.hsa_attention(q[0], k[0], v[0], i, s_i, f, n, 64, 64, c["topk"], c["mode"],
+                                  framewise=True, threads=threads)
+    dt = time.perf_counter() - t0
+    flops = O.effective_flops(sel.bits, O.q_tiling(f, n, 64, True), O.k_tiling(i, f, n, 64, True), d)
+    assert np.isfinite(out).all()
+    return dt, flops
+
+
+def run_reference(args, c):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2602_04789_b200 as lf  # layout helper only (no GPU use)
+    lay = make_layout(lf, c)
+    s_i = host_s(lf, c, lay)
+    threads = os.cpu_count() or 1
+    for w in range(args.warmup):
+        oracle_sample(c, s_i, 100 + w, threads)
+    times, flops = [], []
+    for st in range(args.steps):
+        dt, fl = oracle_sample(c, s_i, 1000 + st, threads)
+        times.append(dt)
+        flops.append(fl)
+    tot_t = sum(times)
+    value = sum(flops) / tot_t / 1e12
+    ms_chunk = statistics.mean(times) * c["heads"] * c["T"] * 1e3
+    sample = (f"1 head of 1 denoising-step call of chunk {c['chunk']} per step (oracle port of "
+              f"chunkattn.hsa_attention, framewise n={c['n']}), OPENBLAS_NUM_THREADS=1, "
+              f"threads={threads}; ms/chunk extrapolated x{c['heads']} heads x{c['T']} steps")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(times) * 1e3, "ms_per_chunk": ms_chunk,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic",
+        "config": {"workload": args.config, **{k: v for k, v in c.items() if k != "plan"},
+                   "plan": list(c["plan"]) if c["plan"] else None, "s_i": s_i},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample, "cpu": cpu_desc()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU leg
+
+
+def run_ours(args, c):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_04789_b200 as lf
+    from paper_2602_04789_b200 import device as D
+    from paper_2602_04789_b200.selection import tilings
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    H, d, f, n, i, T = c["heads"], c["d"], c["f"], c["n"], c["chunk"], c["T"]
+    lay = make_layout(lf, c)
+    cfg = lf.SelectionConfig(topk_frames=c["topk"], block_budget_mode=c["mode"])
+    if world > 1 and H % world == 0:
+        mode, h_local, scaling = "headshard", H // world, "strong"
+    elif world > 1:
+        mode, h_local, scaling = "replica", H, "weak"
+    else:
+        mode, h_local, scaling = "single", H, "weak"
+    h0 = rank * h_local if mode == "headshard" else 0
+
+    # CAG plan solved on device; the selection kernel reads s_i from device memory
+    if c["plan"] is not None:
+        plan = lf.allocate(c["plan"][0], c["plan"][1], c["N"], T, lay)
+        s_dev = plan.device.s[i - 1:i]
+        s_host = plan.s[i - 1]
+    else:
+        s_host = float(c["s"])
+        s_dev = torch.tensor([s_host], dtype=torch.float64, device=dev)
+
+    lq, lk = f * n, i * f * n
+    video = rank if mode == "replica" else 0
+
+    def gen(step, rows, h_start):
+        g = torch.Generator(device=dev)
+        out = torch.empty((h_local, rows, d), dtype=torch.bfloat16, device=dev)
+        for h in range(h_local):
+            g.manual_seed(((video * 64 + step) * 1024 + h_start + h) * 7 + rows)
+            out[h] = torch.randn((rows, d), generator=g, device=dev).to(torch.bfloat16)
+        return out
+
+    Q = [gen(s, lq, h0) for s in range(T)]
+    K = [gen(s + 100, lk, h0) for s in range(T)]
+    V = [gen(s + 200, lk, h0) for s in range(T)]
+    pipes = [lf.HsaPipeline(lay, h_local, i, cfg, framewise=True, out_dtype=torch.bfloat16)
+             for _ in range(T)]
+    outs = [p.bind(Q[s], K[s], V[s], s_dev) for s, p in enumerate(pipes)]
+    full = [torch.empty((H, lq, d), dtype=torch.bfloat16, device=dev) for _ in range(T)] \
+        if mode == "headshard" else None
+
+    def gather(s):
+        if mode == "headshard":
+            dist.all_gather_into_tensor(full[s], outs[s])
+
+    if args.profile_launch:
+        for _ in range(2):
+            for s in range(T):
+                pipes[s].launch()
+        torch.cuda.synchronize()
+        return
+
+    clocks = ClockSampler(local).start()
+    for _ in range(max(args.warmup, 3)):
+        for s in range(T):
+            pipes[s].launch()
+            gather(s)
+    torch.cuda.synchronize()
+    for p in pipes:
+        p.capture()
+    for _ in range(2):
+        for s in range(T):
+            pipes[s].replay()
+            gather(s)
+    torch.cuda.synchronize()
+    errs = sum(p.errors() for p in pipes)
+
+    # effective (selected) FLOPs of one step = T calls, summed over ranks
+    flops_local = sum(p.effective_flops() for p in pipes)
+    fl = torch.tensor([float(flops_local)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(fl)
+    flops_step = float(fl.item())
+
+    # ---- timed region: K steps of graph replays (+ all-gather when sharded)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        for s in range(T):
+            pipes[s].replay()
+            gather(s)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    clk = clocks.stop()
+    value = flops_step / (ms_step * 1e-3) / 1e12
+
+    # ---- kernel-level timing for the roofline (same kernels, same inputs, eager)
+    qt, kt = tilings(lay, i, True)
+    bpf = lay.frame_kv_blocks
+    P = (i - 1) * f
+    stage = {"pool": [], "select": [], "attn": []}
+    reps = max(5, min(args.steps, 50))
+    evs = []
+    for r in range(reps):
+        for s in range(T):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            qb, kb, kf = D.compress(Q[s], K[s], qt, kt, bpf, P)
+            ev[1].record()
+            sel = D.select(qb, kb, kf, bpf, i, f, c["topk"], c["mode"] == "per-frame", s_dev)
+            tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf)
+            ev[2].record()
+            D.attention(Q[s], K[s], V[s], qt, tiles, P * n, lk, out=outs[s])
+            ev[3].record()
+            evs.append(ev)
+    torch.cuda.synchronize()
+    for ev in evs:
+        stage["pool"].append(ev[0].elapsed_time(ev[1]))
+        stage["select"].append(ev[1].elapsed_time(ev[2]))
+        stage["attn"].append(ev[2].elapsed_time(ev[3]))
+    attn_ms = statistics.mean(stage["attn"])
+    pool_ms = statistics.mean(stage["pool"])
+    sel_ms = statistics.mean(stage["select"])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    tf_peak = peaks.get("bf16_tflops", 1590.0)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    flops_call = flops_local / T
+    achieved_tf = flops_call / (attn_ms * 1e-3) / 1e12
+    pool_bytes = h_local * (lq + lk) * d * 2 + h_local * (qt.count + kt.count + P) * d * 4
+    achieved_gbs = pool_bytes / (pool_ms * 1e-3) / 1e9
+
+    # ---- end to end through the C-ABI pipeline with host (pinned) buffers
+    hq = [x.cpu().pin_memory() for x in Q]
+    hk = [x.cpu().pin_memory() for x in K]
+    hv = [x.cpu().pin_memory() for x in V]
+    ho = [torch.empty(outs[s].shape, dtype=outs[s].dtype).pin_memory() for s in range(T)]
+    h2d = sum(x.numel() * 2 for x in hq + hk + hv)
+    d2h = sum(x.numel() * 2 for x in ho)
+    e2e_steps = max(3, min(args.steps, 20))
+
+    def e2e_step():
+        for s in range(T):
+            Q[s].copy_(hq[s], non_blocking=True)
+            K[s].copy_(hk[s], non_blocking=True)
+            V[s].copy_(hv[s], non_blocking=True)
+            pipes[s].replay()
+            gather(s)
+            ho[s].copy_(outs[s], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    b.record()
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / e2e_steps
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    # ---- CPU baseline (rank 0, N = 1 only): oracle on a bounded sample of the same workload
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        dt, cflops = oracle_sample(c, s_host, 4242, threads)
+        cpu = {"value": cflops / dt / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": (f"1 head x 1 denoising-step call of chunk {i} (framewise oracle port "
+                          f"of chunkattn.hsa_attention), {dt:.2f} s; OPENBLAS_NUM_THREADS=1, "
+                          f"threads={threads}"),
+               "ms_per_chunk_extrapolated": dt * H * T * 1e3, "cpu": cpu_desc()}
+
+    # pool(Q+K), pool(k_frame), select, plan_tiles, attention; chunk 1 has no past stages
+    launches_per_call = 5 if P > 0 else 3
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "ms_per_chunk": ms_step, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {H} heads x d{d}, n={n} tokens/frame "
+                                   f"(framewise b=64), f={f}, chunk {i} of {c['N']}, "
+                                   f"T={T} calls/step",
+                       "heads": H, "d": d, "n": n, "f": f, "chunk": i, "N": c["N"],
+                       "plan": list(c["plan"]) if c["plan"] else None, "s_i": s_host,
+                       "topk_frames": c["topk"], "mode": c["mode"], "parallelism": mode,
+                       "l2": "inputs larger than L2 (K+V per call "
+                             f"{2 * h_local * lk * d * 2 / 1e6:.0f} MB)"},
+            "e2e": {"value": flops_step / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
+                    "ms_per_chunk": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel<128>",
+                         "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
+                         "frac": achieved_tf / tf_peak, "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                         "attn_ms_per_call": attn_ms, "flops_per_call": flops_call},
+            "roofline_select": {"bound": "hbm", "kernel": "pool_kernel (Q+K block pooling)",
+                                "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                                "frac": achieved_gbs / hbm_peak, "bytes_per_call": pool_bytes,
+                                "pool_ms_per_call": pool_ms, "select_plan_ms_per_call": sel_ms},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches_per_call * T * args.steps,
+            "device_errors": errs,
+            "effective_flops_per_step": flops_step,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, c)
+    else:
+        run_ours(args, c)
+
+
+if __name__ == "__main__":
+    main()
