@@ -220,6 +220,7 @@ def run_ours(args, c):
     import paper_2602_04789_b200 as lf
     from paper_2602_04789_b200 import device as D
     from paper_2602_04789_b200.selection import tilings
+    from paper_2602_04789_b200.sharding import gather_heads, partition_heads
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -229,13 +230,9 @@ def run_ours(args, c):
     H, d, f, n, i, T = c["heads"], c["d"], c["f"], c["n"], c["chunk"], c["T"]
     lay = make_layout(lf, c)
     cfg = lf.SelectionConfig(topk_frames=c["topk"], block_budget_mode=c["mode"])
-    if world > 1 and H % world == 0:
-        mode, h_local, scaling = "headshard", H // world, "strong"
-    elif world > 1:
-        mode, h_local, scaling = "replica", H, "weak"
-    else:
-        mode, h_local, scaling = "single", H, "weak"
-    h0 = rank * h_local if mode == "headshard" else 0
+    shard = partition_heads(H, world, rank)
+    mode, h_local, h0 = shard.mode, shard.local_heads, shard.h0
+    scaling = "strong" if mode == "headshard" else "weak"
 
     # CAG plan solved on device; the selection kernel reads s_i from device memory
     if c["plan"] is not None:
@@ -268,7 +265,7 @@ def run_ours(args, c):
 
     def gather(s):
         if mode == "headshard":
-            dist.all_gather_into_tensor(full[s], outs[s])
+            gather_heads(outs[s], shard, out=full[s])
 
     if args.profile_launch:
         for _ in range(2):

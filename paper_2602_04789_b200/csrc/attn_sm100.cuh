@@ -237,15 +237,28 @@ __global__ void __launch_bounds__(192, 1) attn_fwd_kernel(const __grid_constant_
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(t_row + C::COL_S + st * 128 + c * 32, s + c * 32);
       tmem_ld_wait();
-      const bool a0 = (ts.m0 >> lq) & 1, a1 = (ts.m1 >> lq) & 1;
-      const int lim0 = a0 ? ts.l0 : 0, lim1 = a1 ? ts.l1 : 0;
-      float mt = -INFINITY;
+      // mask keys outside the row's active segments (only partial tiles pay for it)
+      const bool full = (ts.m0 & ts.m1) == -1 && ts.l0 == 64 && ts.l1 == 64;
+      if (!full) {
+        const bool a0 = (ts.m0 >> lq) & 1, a1 = (ts.m1 >> lq) & 1;
+        const int lim0 = a0 ? ts.l0 : 0, lim1 = a1 ? ts.l1 : 0;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        s[c] = c < lim0 ? s[c] : -INFINITY;
-        s[64 + c] = c < lim1 ? s[64 + c] : -INFINITY;
-        mt = fmaxf(mt, fmaxf(s[c], s[64 + c]));
+        for (int c = 0; c < 64; ++c) {
+          s[c] = c < lim0 ? s[c] : -INFINITY;
+          s[64 + c] = c < lim1 ? s[64 + c] : -INFINITY;
+        }
       }
+      // row max: 3-input max tree (no serial dependency chain)
+      float mx[16];
+#pragma unroll
+      for (int g = 0; g < 16; ++g) {
+        const float* v = s + 8 * g;
+        mx[g] = fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmaxf(v[6], v[7]));
+      }
+      float mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]),
+                       fmax3(mx[6], mx[7], mx[8]));
+      mt = fmax3(mt, fmax3(mx[9], mx[10], mx[11]), fmax3(mx[12], mx[13], mx[14]));
+      mt = fmaxf(mt, mx[15]);
       const float m_new = fmaxf(m_used, mt);
       const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
       const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
@@ -269,11 +282,31 @@ __global__ void __launch_bounds__(192, 1) attn_fwd_kernel(const __grid_constant_
         m_used = m_new;
       }
       const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
+      // x = s*c2 - m*c2 on FFMA2, then 2^x: 3 of every 4 pairs on MUFU, 1 on the FMA pipes
+      const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
+      uint64_t acc[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) acc[g] = 0ull;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        float a, b;
+        f2unpack(ffma2(f2pack(s[2 * c], s[2 * c + 1]), c2v, nm), a, b);
+        if ((c & 3) == 3) {
+          exp2_poly2(a, b);
+        } else {
+          a = ex2(a);
+          b = ex2(b);
+        }
+        s[2 * c] = a;
+        s[2 * c + 1] = b;
+        acc[c & 7] = fadd2(acc[c & 7], f2pack(a, b));
+      }
       float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        s[c] = ex2(fmaf(s[c], c2, -msub));
-        rs += s[c];
+      for (int g = 0; g < 8; ++g) {
+        float a, b;
+        f2unpack(acc[g], a, b);
+        rs += a + b;
       }
       l += rs;
       if (j >= 2) mbar_wait(pv_done + st, ((j - 2) >> 1) & 1);  // P buffer st is free

@@ -207,6 +207,57 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100a)
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// 2^x on the FMA pipes (Cody-Waite split + degree-3 minimax, rel. err 7.5e-5,
+// far below the bf16 rounding of P), for two values at once.  Offloads part
+// of the exponentials from the MUFU unit (16 ex2/clk/SM on B200).
+__device__ __forceinline__ void exp2_poly2(float& a, float& b) {
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  const uint64_t nmagic = f2pack(-12582912.0f, -12582912.0f);
+  uint64_t x = f2pack(a, b);
+  uint64_t t = fadd2(x, magic);            // round-to-nearest integer in the low mantissa bits
+  uint64_t r = fadd2(t, nmagic);           // that integer as a float
+  float rl, rh;
+  f2unpack(r, rl, rh);
+  uint64_t f = fadd2(x, f2pack(-rl, -rh)); // fraction in [-0.5, 0.5]
+  uint64_t p = ffma2(f, f2pack(0.05517084f, 0.05517084f), f2pack(0.24260935f, 0.24260935f));
+  p = ffma2(p, f, f2pack(0.69326096f, 0.69326096f));
+  p = ffma2(p, f, f2pack(0.99992818f, 0.99992818f));
+  float pl, ph, tl, th;
+  f2unpack(p, pl, ph);
+  f2unpack(t, tl, th);
+  // below 2^-126 (and for masked -inf inputs) the result is exactly 0, like ex2.approx.ftz
+  const float ra = __int_as_float(__float_as_int(pl) + (__float_as_int(tl) << 23));
+  const float rb = __int_as_float(__float_as_int(ph) + (__float_as_int(th) << 23));
+  a = a < -126.0f ? 0.0f : ra;
+  b = b < -126.0f ? 0.0f : rb;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);

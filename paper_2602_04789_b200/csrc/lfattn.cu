@@ -1,11 +1,13 @@
 // C ABI of the sm_100a hot path (see include/lfattn.h): argument checking,
 // TMA descriptor encoding, workspace carving and kernel launches.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
 
 #include "attn_sm100.cuh"
+#include "attn_sm100_v2.cuh"
 #include "cag.cuh"
 #include "pool.cuh"
 #include "select.cuh"
@@ -422,6 +424,28 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
   p.out_head_stride = out_head_stride;
   p.lse = lse;
   p.err = err_flag;
+  static const bool use_v1 = getenv("LF_ATTN_V1") != nullptr;
+  if (!use_v1) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const int work = p.n_qtiles * q->heads;
+    const int grid2 = work < 2 * sms ? work : 2 * sms;
+    if (q->d == 128) {
+      cudaFuncSetAttribute(attn_fwd_v2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           AttnCfg2<128>::SMEM);
+      attn_fwd_v2_kernel<128><<<grid2, 192, AttnCfg2<128>::SMEM, S(stream)>>>(p, work);
+    } else {
+      cudaFuncSetAttribute(attn_fwd_v2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           AttnCfg2<64>::SMEM);
+      attn_fwd_v2_kernel<64><<<grid2, 192, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
+    }
+    return check_launch("attn_fwd_v2_kernel");
+  }
   dim3 grid(p.n_qtiles, q->heads);
   if (q->d == 128) {
     cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
