@@ -33,7 +33,7 @@ struct AttnCfg2 {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + KV_BYTES;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int SMEM = OFF_BAR + 128 + 1024 + 1024;  // barriers, row-stat exchange, align
   static constexpr int TMEM_COLS = 256;
   static constexpr int COL_S = 0;    // S fp32 [128 cols]; P bf16 packed over cols [0, 64)
   static constexpr int COL_O = 128;  // O fp32 [D cols]
@@ -98,7 +98,7 @@ __device__ __forceinline__ void mask_chunk(float* v, int c, const TileSegs& ts, 
 }
 
 template <int D>
-__global__ void __launch_bounds__(192, 2) attn_fwd_v2_kernel(const __grid_constant__ AttnParams p,
+__global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_constant__ AttnParams p,
                                                               int total_work) {
   using C = AttnCfg2<D>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_v2_kernel(const __grid_consta
     mbar_init(v_full, 1);
     mbar_init(v_empty, 1);
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(o_full, 1);
     fence_barrier_init();
   }
@@ -218,10 +218,22 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_v2_kernel(const __grid_consta
     __syncwarp();
   } else {
     // ------------------------------------------------------------- softmax + epilogue
+    // 8 warps: warp w (2..9) owns TMEM lane quarter (w & 3) -> query rows
+    // 32*(w&3)..+31, and column half hf = (w - 2) >> 2 of S (keys 64*hf..+63)
+    // and of O (dims D/2*hf..+D/2).  The two warps of a quarter exchange row
+    // maxima through shared memory (named barrier 1 + quarter, 64 threads).
     const int quarter = warp & 3;
+    const int hf = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t s_col = C::COL_S + hf * 64;     // this half's S columns
+    const uint32_t p_col = C::COL_S + hf * 32;     // this half's P columns (bf16 pairs)
+    const uint32_t o_col = C::COL_O + hf * (D / 2);
+    float* red = reinterpret_cast<float*>(bars + 16);  // [2][128] row maxima / sums
     const float c2 = p.scale_log2;
+    auto pair_sync = [&]() {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    };
     uint32_t it = 0, tc = 0;
     for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
       const WorkItem wi = work_item(p, w);
@@ -240,42 +252,29 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_v2_kernel(const __grid_consta
         const bool full = (ts.m0 & ts.m1) == -1 && ts.l0 == 64 && ts.l1 == 64;
         mbar_wait(s_full, it & 1);
         tc_fence_after();
-        // pass 1: row max
-        float mt = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 4; c += 2) {
-          float v[64];
-          tmem_ld32(t_row + C::COL_S + c * 32, v);
-          tmem_ld32(t_row + C::COL_S + c * 32 + 32, v + 32);
-          tmem_ld_wait();
-          if (!full) {
-            mask_chunk(v, c, ts, lq);
-            mask_chunk(v + 32, c + 1, ts, lq);
-          }
-          float mx[8];
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            const float* u = v + 8 * g;
-            mx[g] = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
-          }
-          mt = fmax3(mt, fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]));
-          mt = fmax3(mt, mx[6], mx[7]);
+        float v[64];
+        tmem_ld32(t_row + s_col, v);
+        tmem_ld32(t_row + s_col + 32, v + 32);
+        tmem_ld_wait();
+        if (!full) {
+          mask_chunk(v, 2 * hf, ts, lq);
+          mask_chunk(v + 32, 2 * hf + 1, ts, lq);
         }
+        float mx[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float* u = v + 8 * g;
+          mx[g] = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
+        }
+        float mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]),
+                         fmaxf(mx[6], mx[7]));
+        red[hf * 128 + row] = mt;
+        pair_sync();
+        mt = fmaxf(mt, red[(hf ^ 1) * 128 + row]);
         const float m_new = fmaxf(m_used, mt);
         const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
         const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
-        if (__any_sync(0xffffffffu, need) && j > 0) {
-          // O already holds PV_{0..j-1} (s_full of QK_j committed after them)
-          float o[32];
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            tmem_ld32(t_row + C::COL_O + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= factor;
-            tmem_st32(t_row + C::COL_O + c * 32, o);
-          }
-        }
+        const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
         if (need) {
           l *= factor;
           m_used = m_new;
@@ -283,64 +282,65 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_v2_kernel(const __grid_consta
         const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
         const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        // pass 2: exponentials, P (bf16) written over the consumed S columns
+        // the partner half loaded its S before pair_sync, so P may overwrite it now
 #pragma unroll
-        for (int c = 0; c < 4; c += 2) {
-          float v[64];
-          tmem_ld32(t_row + C::COL_S + c * 32, v);
-          tmem_ld32(t_row + C::COL_S + c * 32 + 32, v + 32);
-          tmem_ld_wait();
-          if (!full) {
-            mask_chunk(v, c, ts, lq);
-            mask_chunk(v + 32, c + 1, ts, lq);
-          }
-          uint32_t pk[32];
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
+          for (int e = 0; e < 16; ++e) {
             float a, b;
-            f2unpack(ffma2(f2pack(v[2 * e], v[2 * e + 1]), c2v, nm), a, b);
-            if ((e & 3) == 3) {
-              exp2_poly2(a, b);
-            } else {
-              a = ex2(a);
-              b = ex2(b);
-            }
+            f2unpack(ffma2(f2pack(v[32 * ch + 2 * e], v[32 * ch + 2 * e + 1]), c2v, nm), a, b);
+            a = ex2(a);
+            b = ex2(b);
             acc[e & 3] = fadd2(acc[e & 3], f2pack(a, b));
             pk[e] = pack_bf16(a, b);
           }
-          tmem_st16(t_row + C::COL_S + c * 16, pk);
-          tmem_st16(t_row + C::COL_S + c * 16 + 16, pk + 16);
+          tmem_st16(t_row + p_col + 16 * ch, pk);
         }
-        float rs = 0.f;
+        if (rescale) {  // after P is out of registers (keeps S and O chunks apart)
+          // O already holds PV_{0..j-1} (s_full of QK_j was committed after them)
+          float o[32];
+#pragma unroll 1
+          for (int c = 0; c < D / 64; ++c) {
+            tmem_ld32(t_row + o_col + c * 32, o);
+            tmem_ld_wait();
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float a, b;
-          f2unpack(acc[g], a, b);
-          rs += a + b;
+            for (int e = 0; e < 32; ++e) o[e] *= factor;
+            tmem_st32(t_row + o_col + c * 32, o);
+          }
         }
-        l += rs;
+        acc[0] = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        float a, b;
+        f2unpack(acc[0], a, b);
+        l += a + b;
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full);
+        pair_sync();  // red[] is reused by the next tile
       }
       if (cx.T == 0) {
         if (row_ok && p.err) atomicOr(p.err, 1);  // no key at all (callers prevent this)
         continue;
       }
-      // epilogue: O / l -> global
+      // epilogue: combine the two halves' partial sums, O / l -> global
+      red[hf * 128 + row] = l;
+      pair_sync();
+      l += red[(hf ^ 1) * 128 + row];
+      pair_sync();
       mbar_wait(o_full, tc++ & 1);
       tc_fence_after();
       const float inv = 1.0f / l;
-      if (row_ok && !(l > 0.f) && p.err) atomicOr(p.err, 1);
+      if (row_ok && hf == 0 && !(l > 0.f) && p.err) atomicOr(p.err, 1);
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 64; ++c) {
         float o[32];
-        tmem_ld32(t_row + C::COL_O + c * 32, o);
+        tmem_ld32(t_row + o_col + c * 32, o);
         tmem_ld_wait();
         if (!row_ok) continue;
+        const int col = hf * (D / 2) + c * 32;
         if (p.out_dtype == LF_F32) {
           float* dst = reinterpret_cast<float*>(p.out) + (long long)wi.h * p.out_head_stride +
-                       (long long)grow * p.out_row_stride + c * 32;
+                       (long long)grow * p.out_row_stride + col;
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
             *reinterpret_cast<float4*>(dst + e) =
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_v2_kernel(const __grid_consta
         } else {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) +
                                (long long)wi.h * p.out_head_stride +
-                               (long long)grow * p.out_row_stride + c * 32;
+                               (long long)grow * p.out_row_stride + col;
 #pragma unroll
           for (int e = 0; e < 32; e += 8)
             *reinterpret_cast<uint4*>(dst + e) = make_uint4(
@@ -356,11 +356,9 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_v2_kernel(const __grid_consta
                 pack_bf16(o[e + 4] * inv, o[e + 5] * inv), pack_bf16(o[e + 6] * inv, o[e + 7] * inv));
         }
       }
-      if (row_ok && p.lse)
+      if (row_ok && hf == 0 && p.lse)
         p.lse[(long long)wi.h * p.Lq + grow] =
             (m_used == -INFINITY ? -INFINITY : m_used * p.scale) + logf(l);
-      // O may be overwritten by the next tile's first PV only after these loads:
-      // the next p_full arrive (after this point) orders it.
       tc_fence_before();
     }
   }

@@ -438,11 +438,11 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
     if (q->d == 128) {
       cudaFuncSetAttribute(attn_fwd_v2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            AttnCfg2<128>::SMEM);
-      attn_fwd_v2_kernel<128><<<grid2, 192, AttnCfg2<128>::SMEM, S(stream)>>>(p, work);
+      attn_fwd_v2_kernel<128><<<grid2, 320, AttnCfg2<128>::SMEM, S(stream)>>>(p, work);
     } else {
       cudaFuncSetAttribute(attn_fwd_v2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            AttnCfg2<64>::SMEM);
-      attn_fwd_v2_kernel<64><<<grid2, 192, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
+      attn_fwd_v2_kernel<64><<<grid2, 320, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
     }
     return check_launch("attn_fwd_v2_kernel");
   }
