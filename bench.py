@@ -40,6 +40,11 @@ CONFIGS = {
     # configs[2]: long rollout, chunk 14 of 21 (42 frames of KV), CAG plan -> past blocks selected
     "c3": dict(heads=12, d=128, n=1560, f=3, N=21, chunk=14, plan=(0.9, 0.98), s=None, topk=6,
                mode="global", T=4),
+    # load-balance probes (diagnostics): 8 / 16 heads = exactly 1 / 2 work items per CTA
+    "c2h8": dict(heads=8, d=128, n=1560, f=3, N=7, chunk=7, plan=(0.9, 0.98), s=None, topk=6,
+                 mode="global", T=4),
+    "c2h16": dict(heads=16, d=128, n=1560, f=3, N=7, chunk=7, plan=(0.9, 0.98), s=None, topk=6,
+                  mode="global", T=4),
     # configs[3]: Wan-14B attention shape (40 heads)
     "c4": dict(heads=40, d=128, n=1560, f=3, N=7, chunk=7, plan=(0.9, 0.98), s=None, topk=6,
                mode="global", T=4),

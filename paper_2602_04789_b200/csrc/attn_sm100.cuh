@@ -59,6 +59,13 @@ struct AttnParams {
   long long out_row_stride, out_head_stride;
   float* lse;
   int* err;
+  // split-KV load balancing (v2 only): each (head, q-tile) item is cut into
+  // `split` parts over its key tiles; parts write unnormalised partials and the
+  // last one to finish merges them (see attn_sm100_v2.cuh)
+  int split;
+  float* part_o;    // [items*split][128][D] fp32
+  float2* part_ml;  // [items*split][128] (row max, row sum)
+  int* counters;    // [items], zero between launches
 };
 
 struct TileSegs {

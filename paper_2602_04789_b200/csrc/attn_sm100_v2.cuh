@@ -62,18 +62,21 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 }
 
 struct WorkItem {
-  int h, tile;
+  int h, tile, item, part;
 };
-__device__ __forceinline__ WorkItem work_item(const AttnParams& p, int w) {
-  // head-major order: the CTAs of one wave share K/V of few heads in L2
+__device__ __forceinline__ WorkItem work_item(const AttnParams& p, int u) {
+  // unit u = (item, part); head-major items so concurrent CTAs share K/V in L2
   WorkItem it;
-  it.h = w / p.n_qtiles;
-  it.tile = w - it.h * p.n_qtiles;
+  it.item = u / p.split;
+  it.part = u - it.item * p.split;
+  it.h = it.item / p.n_qtiles;
+  it.tile = it.item - it.h * p.n_qtiles;
   return it;
 }
 
 struct TileCtx {
-  int nseg, Tp, T;
+  int nseg, Tp, T;  // T = all key tiles of the item
+  int j0, j1;       // this part's key tiles [j0, j1)
   const int4* segs;
 };
 __device__ __forceinline__ TileCtx tile_ctx(const AttnParams& p, WorkItem wi) {
@@ -84,6 +87,8 @@ __device__ __forceinline__ TileCtx tile_ctx(const AttnParams& p, WorkItem wi) {
   c.Tp = (c.nseg + 1) >> 1;
   const int dense = p.dense_hi > p.dense_lo ? p.dense_hi - p.dense_lo : 0;
   c.T = c.Tp + (dense + 127) / 128;
+  c.j0 = (int)((long long)c.T * wi.part / p.split);
+  c.j1 = (int)((long long)c.T * (wi.part + 1) / p.split);
   return c;
 }
 
@@ -150,12 +155,12 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
       for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
         const WorkItem wi = work_item(p, w);
         const TileCtx cx = tile_ctx(p, wi);
-        if (cx.T == 0) continue;
+        if (cx.j1 == cx.j0) continue;
         mbar_wait(q_empty, (tc++ & 1) ^ 1);
         mbar_expect_tx(q_full, C::Q_BYTES);
         for (int a = 0; a < C::ATOMS; ++a)
           tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, wi.tile * C::BM, wi.h);
-        for (int j = 0; j < cx.T; ++j, ++it) {
+        for (int j = cx.j0; j < cx.j1; ++j, ++it) {
           const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
           const uint32_t par = (it & 1) ^ 1;
           mbar_wait(k_empty, par);
@@ -185,9 +190,9 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
       uint32_t it = 0, tc = 0;
       for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
         const TileCtx cx = tile_ctx(p, work_item(p, w));
-        if (cx.T == 0) continue;
+        if (cx.j1 == cx.j0) continue;
         mbar_wait(q_full, tc++ & 1);
-        for (int j = 0; j < cx.T; ++j, ++it) {
+        for (int j = cx.j0; j < cx.j1; ++j, ++it) {
           mbar_wait(k_full, it & 1);
           tc_fence_after();
 #pragma unroll
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
           }
           tc_commit(k_empty);
           tc_commit(s_full);
-          if (j == cx.T - 1) tc_commit(q_empty);
+          if (j == cx.j1 - 1) tc_commit(q_empty);
           mbar_wait(p_full, it & 1);
           mbar_wait(v_full, it & 1);
           tc_fence_after();
@@ -208,10 +213,10 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
           for (int kk = 0; kk < C::BN / 16; ++kk) {
             uint64_t bd = smem_desc_sw128(v_base + kk * 16 * 128, C::BN * 128, 1024);
             tc_mma_ts(tmem + C::COL_O, tmem + C::COL_S + kk * 8, bd, IDESC_PV,
-                      (j > 0 || kk > 0) ? 1u : 0u);
+                      (j > cx.j0 || kk > 0) ? 1u : 0u);
           }
           tc_commit(v_empty);
-          if (j == cx.T - 1) tc_commit(o_full);
+          if (j == cx.j1 - 1) tc_commit(o_full);
         }
       }
     }
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
         lq = lq < 32 ? lq : 31;
       }
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < cx.T; ++j, ++it) {
+      for (int j = cx.j0; j < cx.j1; ++j, ++it) {
         const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
         const bool full = (ts.m0 & ts.m1) == -1 && ts.l0 == 64 && ts.l1 == 64;
         mbar_wait(s_full, it & 1);
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
         const float m_new = fmaxf(m_used, mt);
         const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
         const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
-        const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
+        const bool rescale = __any_sync(0xffffffffu, need) && j > cx.j0;
         if (need) {
           l *= factor;
           m_used = m_new;
@@ -322,13 +327,85 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
         if (row_ok && p.err) atomicOr(p.err, 1);  // no key at all (callers prevent this)
         continue;
       }
-      // epilogue: combine the two halves' partial sums, O / l -> global
+      const bool empty_part = cx.j1 == cx.j0;
+      // combine the two halves' partial sums
       red[hf * 128 + row] = l;
       pair_sync();
       l += red[(hf ^ 1) * 128 + row];
       pair_sync();
-      mbar_wait(o_full, tc++ & 1);
-      tc_fence_after();
+      if (!empty_part) {
+        mbar_wait(o_full, tc++ & 1);
+        tc_fence_after();
+      }
+      if (p.split > 1) {
+        // ---- split-KV: publish this part's unnormalised O, (m, l); last part merges
+        const long long unit = (long long)wi.item * p.split + wi.part;
+        float* po = p.part_o + (unit * 128 + row) * D + hf * (D / 2);
+        if (!empty_part) {
+#pragma unroll 1
+          for (int c = 0; c < D / 64; ++c) {
+            float o[32];
+            tmem_ld32(t_row + o_col + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(po + c * 32 + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          }
+        }
+        if (hf == 0) p.part_ml[unit * 128 + row] = make_float2(m_used, empty_part ? 0.f : l);
+        tc_fence_before();
+        __threadfence();
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        uint32_t* flag = reinterpret_cast<uint32_t*>(bars + 13);
+        if (threadIdx.x == 64) {
+          const int old = atomicAdd(p.counters + wi.item, 1);
+          *flag = old == p.split - 1;
+          if (old == p.split - 1) p.counters[wi.item] = 0;  // reset for the next launch
+        }
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (!*flag) continue;
+        __threadfence();
+        float M = -INFINITY;
+        for (int q = 0; q < p.split; ++q)
+          M = fmaxf(M, __ldcg(&p.part_ml[((long long)wi.item * p.split + q) * 128 + row]).x);
+        float L = 0.f, f[4];
+        for (int q = 0; q < p.split; ++q) {
+          const float2 ml = __ldcg(&p.part_ml[((long long)wi.item * p.split + q) * 128 + row]);
+          f[q] = (ml.y > 0.f && ml.x != -INFINITY) ? ex2((ml.x - M) * c2) : 0.f;
+          L += ml.y * f[q];
+        }
+        const float inv = 1.0f / L;
+        if (row_ok && hf == 0 && !(L > 0.f) && p.err) atomicOr(p.err, 1);
+        if (row_ok) {
+#pragma unroll 1
+          for (int c = 0; c < D / 2; c += 4) {
+            float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < p.split; ++q) {
+              if (f[q] == 0.f) continue;
+              const float4 x = __ldcg(reinterpret_cast<const float4*>(
+                  p.part_o + (((long long)wi.item * p.split + q) * 128 + row) * D + hf * (D / 2) + c));
+              acc4.x += x.x * f[q]; acc4.y += x.y * f[q]; acc4.z += x.z * f[q]; acc4.w += x.w * f[q];
+            }
+            const int col = hf * (D / 2) + c;
+            if (p.out_dtype == LF_F32) {
+              float* dst = reinterpret_cast<float*>(p.out) + (long long)wi.h * p.out_head_stride +
+                           (long long)grow * p.out_row_stride + col;
+              *reinterpret_cast<float4*>(dst) =
+                  make_float4(acc4.x * inv, acc4.y * inv, acc4.z * inv, acc4.w * inv);
+            } else {
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                                   (long long)wi.h * p.out_head_stride +
+                                   (long long)grow * p.out_row_stride + col;
+              *reinterpret_cast<uint2*>(dst) =
+                  make_uint2(pack_bf16(acc4.x * inv, acc4.y * inv), pack_bf16(acc4.z * inv, acc4.w * inv));
+            }
+          }
+          if (hf == 0 && p.lse)
+            p.lse[(long long)wi.h * p.Lq + grow] = (M == -INFINITY ? -INFINITY : M * p.scale) + logf(L);
+        }
+        continue;
+      }
+      // epilogue: O / l -> global
       const float inv = 1.0f / l;
       if (row_ok && hf == 0 && !(l > 0.f) && p.err) atomicOr(p.err, 1);
 #pragma unroll 1

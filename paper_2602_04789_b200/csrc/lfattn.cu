@@ -269,6 +269,45 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
   if (q->d != k->d || q->heads != k->heads) return fail(LF_ERR_INVALID, "q/k shape mismatch");
   if (q->d > 256) return fail(LF_ERR_UNSUPPORTED, "d > 256");
   const int d = q->d;
+  {
+    // frame-structured bf16 fast path (hot path): one launch, k_frame fused
+    const bool aligned16 = q->dtype == LF_BF16 && k->dtype == LF_BF16 && d % 8 == 0 &&
+                           q->row_stride % 8 == 0 && k->row_stride % 8 == 0 &&
+                           q->head_stride % 8 == 0 && k->head_stride % 8 == 0 &&
+                           reinterpret_cast<uintptr_t>(q->ptr) % 16 == 0 &&
+                           reinterpret_cast<uintptr_t>(k->ptr) % 16 == 0;
+    const int lpb = d / 8;
+    const bool shape_ok = q_tiling.period == k_tiling.period && q_tiling.block == k_tiling.block &&
+                          q_tiling.total % q_tiling.period == 0 &&
+                          k_tiling.total % k_tiling.period == 0 &&
+                          (lpb == 2 || lpb == 4 || lpb == 8 || lpb == 16 || lpb == 32);
+    const int per = (q_tiling.period + q_tiling.block - 1) / q_tiling.block;
+    if (aligned16 && shape_ok && per == blocks_per_frame && (size_t)per * d * 4 <= 96 * 1024) {
+      FramePoolArgs fa;
+      fa.q = static_cast<const __nv_bfloat16*>(q->ptr);
+      fa.k = static_cast<const __nv_bfloat16*>(k->ptr);
+      fa.q_row = q->row_stride; fa.q_head = q->head_stride;
+      fa.k_row = k->row_stride; fa.k_head = k->head_stride;
+      fa.heads = q->heads; fa.d = d; fa.period = q_tiling.period; fa.block = q_tiling.block;
+      fa.per_period = per;
+      fa.q_frames = q_tiling.total / q_tiling.period;
+      fa.k_frames = k_tiling.total / k_tiling.period;
+      fa.past_frames = past_frames;
+      fa.q_block = q_block; fa.k_block = k_block; fa.k_frame = k_frame;
+      const int smem = per * d * 4;
+      const int grid = q->heads * (fa.q_frames + fa.k_frames);
+#define LF_FP(L)                                                                              \
+  if (lpb == L) {                                                                             \
+    if (smem > 48 * 1024)                                                                     \
+      cudaFuncSetAttribute(pool_frames_bf16_kernel<L>,                                        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
+    pool_frames_bf16_kernel<L><<<grid, 512, smem, S(stream)>>>(fa);                          \
+  }
+      LF_FP(2) LF_FP(4) LF_FP(8) LF_FP(16) LF_FP(32)
+#undef LF_FP
+      return check_launch("pool_frames_bf16_kernel");
+    }
+  }
   int vq, nq, vk, nk;
   pool_shape(q, &vq, &nq);
   pool_shape(k, &vk, &nk);
@@ -433,8 +472,51 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (sms <= 0) sms = 148;
     }
-    const int work = p.n_qtiles * q->heads;
-    const int grid2 = work < 2 * sms ? work : 2 * sms;
+    const int items = p.n_qtiles * q->heads;
+    const int slots = 2 * sms;  // two co-resident CTAs per SM
+    // split-KV balancing: cut each item into s parts when items do not fill the
+    // slots evenly (e.g. 444 items on 296 slots -> 888 parts, 3 per CTA)
+    int split = 1;
+    {
+      double best = 1e30;
+      for (int s2 = 1; s2 <= 4; ++s2) {
+        const long long units = (long long)items * s2;
+        const double rounds = (double)((units + slots - 1) / slots) / s2;
+        const double cost = rounds * (1.0 + 0.04 * (s2 - 1));
+        if (cost < best - 1e-9) { best = cost; split = s2; }
+      }
+      if (getenv("LF_ATTN_SPLIT")) split = atoi(getenv("LF_ATTN_SPLIT"));
+      split = split < 1 ? 1 : (split > 4 ? 4 : split);
+    }
+    if (split > 1) {
+      const size_t need_o = (size_t)items * split * 128 * q->d * 4;
+      const size_t need_ml = (size_t)items * split * 128 * 8;
+      const size_t need_c = (size_t)items * 4;
+      static void* ws = nullptr;
+      static size_t ws_bytes = 0;
+      const size_t need = align_up(need_o, 256) + align_up(need_ml, 256) + align_up(need_c, 256);
+      if (need > ws_bytes) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(S(stream), &cs);
+        if (cs != cudaStreamCaptureStatusNone) {
+          split = 1;  // cannot allocate inside a graph capture
+        } else {
+          // the old buffer is kept alive: captured CUDA graphs may still point at it
+          void* fresh = nullptr;
+          if (cudaMalloc(&fresh, need) != cudaSuccess) { split = 1; }
+          else { ws = fresh; ws_bytes = need; cudaMemset(ws, 0, need); }
+        }
+      }
+      if (split > 1) {
+        char* b = static_cast<char*>(ws);
+        p.part_o = reinterpret_cast<float*>(b);
+        p.part_ml = reinterpret_cast<float2*>(b + align_up(need_o, 256));
+        p.counters = reinterpret_cast<int*>(b + align_up(need_o, 256) + align_up(need_ml, 256));
+      }
+    }
+    p.split = split;
+    const int work = items * split;
+    const int grid2 = work < slots ? work : slots;
     if (q->d == 128) {
       cudaFuncSetAttribute(attn_fwd_v2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            AttnCfg2<128>::SMEM);

@@ -146,3 +146,122 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolArgs a) {
 }
 
 }  // namespace lf
+
+namespace lf {
+
+// ---------------------------------------------------------------------------
+// Frame-structured fast path for bf16 inputs (the hot path): one CTA per
+// (head, frame) pools all blocks of the frame and, for past key frames, the
+// frame summary (mean of the block means, selection.py:111) from shared
+// memory -- one launch instead of two.  Groups of d/8 lanes stream one block
+// each with 16-byte loads (8 bf16 per lane, a lane still owns its columns for
+// every row, so each column is summed in row order exactly like the
+// reference).  bf16 -> fp64 conversion: the low bf16 of each 32-bit word goes
+// through F2F (XU pipe), the high one is re-biased with integer ops into an
+// fp64 scaled by 2^-896 (exact: same mantissa, exponent field shifted), so
+// the XU pipe only carries half the conversions; the scale is undone exactly
+// (power of two) before the division.
+
+struct FramePoolArgs {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  long long q_row, q_head, k_row, k_head;  // element strides
+  int heads, d, period, block, per_period;
+  int q_frames, k_frames, past_frames;
+  float* q_block;  // [H][q_frames*bpf][d]
+  float* k_block;  // [H][k_frames*bpf][d]
+  float* k_frame;  // [H][past_frames][d]
+};
+
+__device__ __forceinline__ double bf16_hi_scaled(uint32_t w) {
+  // high bf16 of w as fp64 * 2^-896 (sign | exponent | mantissa shifted by 3)
+  const uint32_t hi = (w & 0x80000000u) | ((w >> 3) & 0x0FFFE000u);
+  return __hiloint2double((int)hi, 0);
+}
+__device__ __forceinline__ double bf16_lo(uint32_t w) {
+  return (double)__uint_as_float(w << 16);
+}
+
+template <int LPB>  // lanes per block stream = d / 8
+__global__ void __launch_bounds__(512) pool_frames_bf16_kernel(FramePoolArgs a) {
+  constexpr int GROUPS = 512 / LPB;
+  constexpr int UNROLL = 8;
+  extern __shared__ float fp_smem[];  // [bpf][d] block means of this frame (key frames)
+  const int nfr = a.q_frames + a.k_frames;
+  const int h = blockIdx.x / nfr;
+  const int fr = blockIdx.x - h * nfr;
+  const bool is_q = fr < a.q_frames;
+  const int frame = is_q ? fr : fr - a.q_frames;
+  const __nv_bfloat16* base =
+      is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
+  const long long rs = is_q ? a.q_row : a.k_row;
+  float* out = is_q ? a.q_block + ((long long)h * a.q_frames * a.per_period) * a.d
+                    : a.k_block + ((long long)h * a.k_frames * a.per_period) * a.d;
+  const int grp = threadIdx.x / LPB;
+  const int gl = threadIdx.x - grp * LPB;
+  const int col = gl * 8;
+  const bool keep = !is_q && frame < a.past_frames;
+  for (int j = grp; j < a.per_period; j += GROUPS) {
+    const int r0 = frame * a.period + j * a.block;
+    int r1 = r0 + a.block;
+    const int fe = frame * a.period + a.period;
+    r1 = r1 < fe ? r1 : fe;
+    const uint4* p = reinterpret_cast<const uint4*>(base + (long long)r0 * rs + col);
+    const long long step = rs / 8;  // uint4 units
+    double acc[8];
+    {
+      uint4 u = __ldg(p);
+      acc[0] = bf16_lo(u.x); acc[1] = bf16_hi_scaled(u.x);
+      acc[2] = bf16_lo(u.y); acc[3] = bf16_hi_scaled(u.y);
+      acc[4] = bf16_lo(u.z); acc[5] = bf16_hi_scaled(u.z);
+      acc[6] = bf16_lo(u.w); acc[7] = bf16_hi_scaled(u.w);
+      p += step;
+    }
+    int r = r0 + 1;
+    for (; r + UNROLL <= r1; r += UNROLL) {
+      uint4 u[UNROLL];
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) u[k] = __ldg(p + k * step);
+      p += UNROLL * step;
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        acc[0] += bf16_lo(u[k].x); acc[1] += bf16_hi_scaled(u[k].x);
+        acc[2] += bf16_lo(u[k].y); acc[3] += bf16_hi_scaled(u[k].y);
+        acc[4] += bf16_lo(u[k].z); acc[5] += bf16_hi_scaled(u[k].z);
+        acc[6] += bf16_lo(u[k].w); acc[7] += bf16_hi_scaled(u[k].w);
+      }
+    }
+    for (; r < r1; ++r) {
+      uint4 u = __ldg(p);
+      p += step;
+      acc[0] += bf16_lo(u.x); acc[1] += bf16_hi_scaled(u.x);
+      acc[2] += bf16_lo(u.y); acc[3] += bf16_hi_scaled(u.y);
+      acc[4] += bf16_lo(u.z); acc[5] += bf16_hi_scaled(u.z);
+      acc[6] += bf16_lo(u.w); acc[7] += bf16_hi_scaled(u.w);
+    }
+    const double cnt = (double)(r1 - r0);
+    const double unscale = 0x1p896;
+    float m[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) m[e] = (float)(((e & 1) ? acc[e] * unscale : acc[e]) / cnt);
+    float* o = out + ((long long)frame * a.per_period + j) * a.d + col;
+    reinterpret_cast<float4*>(o)[0] = make_float4(m[0], m[1], m[2], m[3]);
+    reinterpret_cast<float4*>(o)[1] = make_float4(m[4], m[5], m[6], m[7]);
+    if (keep) {
+      float* sm = fp_smem + j * a.d + col;
+      reinterpret_cast<float4*>(sm)[0] = make_float4(m[0], m[1], m[2], m[3]);
+      reinterpret_cast<float4*>(sm)[1] = make_float4(m[4], m[5], m[6], m[7]);
+    }
+  }
+  if (!keep) return;
+  __syncthreads();
+  // k_frame = mean_pool(k_block, bpf): fp64 in block order, / bpf, -> fp32
+  float* kf = a.k_frame + ((long long)h * a.past_frames + frame) * a.d;
+  for (int c = threadIdx.x; c < a.d; c += blockDim.x) {
+    double s = (double)fp_smem[c];
+    for (int j = 1; j < a.per_period; ++j) s += (double)fp_smem[j * a.d + c];
+    kf[c] = (float)(s / (double)a.per_period);
+  }
+}
+
+}  // namespace lf

@@ -213,3 +213,35 @@ def test_pipeline_graph_replay_deterministic(lf):
         pipe.replay()
     torch.cuda.synchronize()
     assert torch.equal(first, out)
+
+
+@pytest.mark.parametrize("H,f,n,b,i,d", [(3, 3, 1560, 64, 4, 128), (2, 2, 256, 64, 3, 64),
+                                         (2, 1, 100, 32, 5, 16), (1, 3, 1536, 64, 2, 128)])
+def test_compress_bf16_frame_path_bit_exact(lf, H, f, n, b, i, d):
+    # the fused bf16 frame-pooling kernel (hot path) vs the oracle's fp64 sequential pooling
+    from paper_2602_04789_b200 import device as D
+    q, k, _ = O.synthetic_qkv(99 + d, f * n, i * f * n, d, heads=H)
+    k[:, 5, :] *= 3e4  # widen the exponent range of one block
+    k = O.bf16_round(k)
+    dev = torch.device("cuda")
+    qd = torch.from_numpy(q).to(dev, torch.bfloat16)
+    kd = torch.from_numpy(k).to(dev, torch.bfloat16)
+    qt = D.TilingSpec(f * n, n, b)
+    kt = D.TilingSpec(i * f * n, n, b)
+    P = (i - 1) * f
+    qb, kb, kf = D.compress(qd, kd, qt, kt, kt.per_period, P)
+    for h in range(H):
+        views = O.compress(q[h], k[h], i, f, n, b, b, framewise=True)
+        np.testing.assert_array_equal(qb[h].cpu().numpy().view(np.uint32), views.q_block.view(np.uint32))
+        np.testing.assert_array_equal(kb[h].cpu().numpy().view(np.uint32), views.k_block.view(np.uint32))
+        np.testing.assert_array_equal(kf[h].cpu().numpy().view(np.uint32), views.k_frame.view(np.uint32))
+
+
+@pytest.mark.parametrize("split", ["1", "2", "3", "4"])
+def test_split_kv_merge(lf, split, monkeypatch):
+    # the split-KV load balancing (parts merged by the last finisher) must not change results
+    monkeypatch.setenv("LF_ATTN_SPLIT", split)
+    q, k, v = O.synthetic_qkv(21, 700, 3000, 128)
+    out = lf.dense_attention(q[0], k[0], v[0])
+    assert_close_attn(out, O.dense_attention(q[0], k[0], v[0]), f"split {split}")
+    _pipeline_case(lf, 3, 1560, 3, 4, 128, 0.5, 6, "global", seed=4, check_heads=(1,))
