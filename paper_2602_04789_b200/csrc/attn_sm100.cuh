@@ -59,13 +59,14 @@ struct AttnParams {
   long long out_row_stride, out_head_stride;
   float* lse;
   int* err;
-  // split-KV load balancing (v2 only): each (head, q-tile) item is cut into
-  // `split` parts over its key tiles; parts write unnormalised partials and the
-  // last one to finish merges them (see attn_sm100_v2.cuh)
-  int split;
-  float* part_o;    // [items*split][128][D] fp32
-  float2* part_ml;  // [items*split][128] (row max, row sum)
-  int* counters;    // [items], zero between launches
+  // split-KV load balancing (v2 only): items [0, full_items) run whole; each
+  // of the remaining "tail" items is cut into tail_split parts over its key
+  // tiles, the parts write unnormalised partials and the last one to finish
+  // merges them (see attn_sm100_v2.cuh)
+  int full_items, tail_split;
+  float* part_o;    // [tail*tail_split][128][D] fp32
+  float2* part_ml;  // [tail*tail_split][128] (row max, row sum)
+  int* counters;    // [tail], zero between launches
 };
 
 struct TileSegs {

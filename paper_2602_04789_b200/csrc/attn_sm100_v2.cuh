@@ -62,13 +62,24 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 }
 
 struct WorkItem {
-  int h, tile, item, part;
+  int h, tile, item, part, nparts, slot;  // slot: tail index (parts share counters[slot])
 };
 __device__ __forceinline__ WorkItem work_item(const AttnParams& p, int u) {
-  // unit u = (item, part); head-major items so concurrent CTAs share K/V in L2
+  // unit u: whole item u, or part of a tail item; head-major items so
+  // concurrent CTAs share K/V in L2
   WorkItem it;
-  it.item = u / p.split;
-  it.part = u - it.item * p.split;
+  if (u < p.full_items) {
+    it.item = u;
+    it.part = 0;
+    it.nparts = 1;
+    it.slot = 0;
+  } else {
+    const int t = u - p.full_items;
+    it.slot = t / p.tail_split;
+    it.part = t - it.slot * p.tail_split;
+    it.item = p.full_items + it.slot;
+    it.nparts = p.tail_split;
+  }
   it.h = it.item / p.n_qtiles;
   it.tile = it.item - it.h * p.n_qtiles;
   return it;
@@ -87,8 +98,8 @@ __device__ __forceinline__ TileCtx tile_ctx(const AttnParams& p, WorkItem wi) {
   c.Tp = (c.nseg + 1) >> 1;
   const int dense = p.dense_hi > p.dense_lo ? p.dense_hi - p.dense_lo : 0;
   c.T = c.Tp + (dense + 127) / 128;
-  c.j0 = (int)((long long)c.T * wi.part / p.split);
-  c.j1 = (int)((long long)c.T * (wi.part + 1) / p.split);
+  c.j0 = (int)((long long)c.T * wi.part / wi.nparts);
+  c.j1 = (int)((long long)c.T * (wi.part + 1) / wi.nparts);
   return c;
 }
 
@@ -337,9 +348,9 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
         mbar_wait(o_full, tc++ & 1);
         tc_fence_after();
       }
-      if (p.split > 1) {
+      if (wi.nparts > 1) {
         // ---- split-KV: publish this part's unnormalised O, (m, l); last part merges
-        const long long unit = (long long)wi.item * p.split + wi.part;
+        const long long unit = (long long)wi.slot * wi.nparts + wi.part;
         float* po = p.part_o + (unit * 128 + row) * D + hf * (D / 2);
         if (!empty_part) {
 #pragma unroll 1
@@ -358,19 +369,20 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
         asm volatile("bar.sync 5, 256;" ::: "memory");
         uint32_t* flag = reinterpret_cast<uint32_t*>(bars + 13);
         if (threadIdx.x == 64) {
-          const int old = atomicAdd(p.counters + wi.item, 1);
-          *flag = old == p.split - 1;
-          if (old == p.split - 1) p.counters[wi.item] = 0;  // reset for the next launch
+          const int old = atomicAdd(p.counters + wi.slot, 1);
+          *flag = old == wi.nparts - 1;
+          if (old == wi.nparts - 1) p.counters[wi.slot] = 0;  // reset for the next launch
         }
         asm volatile("bar.sync 5, 256;" ::: "memory");
         if (!*flag) continue;
         __threadfence();
         float M = -INFINITY;
-        for (int q = 0; q < p.split; ++q)
-          M = fmaxf(M, __ldcg(&p.part_ml[((long long)wi.item * p.split + q) * 128 + row]).x);
+        const long long base_unit = (long long)wi.slot * wi.nparts;
+        for (int q = 0; q < wi.nparts; ++q)
+          M = fmaxf(M, __ldcg(&p.part_ml[(base_unit + q) * 128 + row]).x);
         float L = 0.f, f[4];
-        for (int q = 0; q < p.split; ++q) {
-          const float2 ml = __ldcg(&p.part_ml[((long long)wi.item * p.split + q) * 128 + row]);
+        for (int q = 0; q < wi.nparts; ++q) {
+          const float2 ml = __ldcg(&p.part_ml[(base_unit + q) * 128 + row]);
           f[q] = (ml.y > 0.f && ml.x != -INFINITY) ? ex2((ml.x - M) * c2) : 0.f;
           L += ml.y * f[q];
         }
@@ -380,10 +392,10 @@ __global__ void __launch_bounds__(320, 2) attn_fwd_v2_kernel(const __grid_consta
 #pragma unroll 1
           for (int c = 0; c < D / 2; c += 4) {
             float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int q = 0; q < p.split; ++q) {
+            for (int q = 0; q < wi.nparts; ++q) {
               if (f[q] == 0.f) continue;
               const float4 x = __ldcg(reinterpret_cast<const float4*>(
-                  p.part_o + (((long long)wi.item * p.split + q) * 128 + row) * D + hf * (D / 2) + c));
+                  p.part_o + ((base_unit + q) * 128 + row) * D + hf * (D / 2) + c));
               acc4.x += x.x * f[q]; acc4.y += x.y * f[q]; acc4.z += x.z * f[q]; acc4.w += x.w * f[q];
             }
             const int col = hf * (D / 2) + c;

@@ -474,48 +474,53 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
     }
     const int items = p.n_qtiles * q->heads;
     const int slots = 2 * sms;  // two co-resident CTAs per SM
-    // split-KV balancing: cut each item into s parts when items do not fill the
-    // slots evenly (e.g. 444 items on 296 slots -> 888 parts, 3 per CTA)
-    int split = 1;
-    {
-      double best = 1e30;
-      for (int s2 = 1; s2 <= 4; ++s2) {
-        const long long units = (long long)items * s2;
-        const double rounds = (double)((units + slots - 1) / slots) / s2;
-        const double cost = rounds * (1.0 + 0.04 * (s2 - 1));
-        if (cost < best - 1e-9) { best = cost; split = s2; }
-      }
-      if (getenv("LF_ATTN_SPLIT")) split = atoi(getenv("LF_ATTN_SPLIT"));
-      split = split < 1 ? 1 : (split > 4 ? 4 : split);
+    // split-KV balancing of the last, partial round: with items = k*slots + rem,
+    // the rem tail items are cut into s = slots/rem (<= 4) parts so every CTA
+    // finishes at about the same time (444 items on 296 slots: 296 whole items
+    // + 148 items in 2 parts).  Small problems (items < slots) split all items.
+    int rem = items >= slots ? items % slots : items;
+    int tail_split = rem ? slots / rem : 1;
+    tail_split = tail_split > 4 ? 4 : tail_split;
+    if (const char* e = getenv("LF_ATTN_SPLIT")) {  // test hook: split every item
+      tail_split = atoi(e);
+      tail_split = tail_split < 1 ? 1 : (tail_split > 4 ? 4 : tail_split);
+      rem = items;
     }
-    if (split > 1) {
-      const size_t need_o = (size_t)items * split * 128 * q->d * 4;
-      const size_t need_ml = (size_t)items * split * 128 * 8;
-      const size_t need_c = (size_t)items * 4;
+    if (tail_split < 2) { rem = 0; tail_split = 1; }
+    if (rem > 0) {
+      // workspace layout: [counters][part_ml][part_o]; counters stay at offset 0
+      // (zeroed once, reset by every merge), so any reuse keeps them valid
       static void* ws = nullptr;
-      static size_t ws_bytes = 0;
-      const size_t need = align_up(need_o, 256) + align_up(need_ml, 256) + align_up(need_c, 256);
-      if (need > ws_bytes) {
+      static size_t cap_c = 0, cap_ml = 0, cap_o = 0;
+      const size_t need_c = align_up((size_t)rem * 4, 256);
+      const size_t need_ml = align_up((size_t)rem * tail_split * 128 * 8, 256);
+      const size_t need_o = (size_t)rem * tail_split * 128 * q->d * 4;
+      if (need_c > cap_c || need_ml > cap_ml || need_o > cap_o) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(S(stream), &cs);
-        if (cs != cudaStreamCaptureStatusNone) {
-          split = 1;  // cannot allocate inside a graph capture
+        void* fresh = nullptr;
+        const size_t nc = need_c > cap_c ? need_c : cap_c, nm = need_ml > cap_ml ? need_ml : cap_ml,
+                     no = need_o > cap_o ? need_o : cap_o;
+        // (the old buffer is kept alive: captured CUDA graphs may still point at it)
+        if (cs == cudaStreamCaptureStatusNone && cudaMalloc(&fresh, nc + nm + no) == cudaSuccess) {
+          cudaMemsetAsync(fresh, 0, nc, S(stream));
+          ws = fresh;
+          cap_c = nc; cap_ml = nm; cap_o = no;
         } else {
-          // the old buffer is kept alive: captured CUDA graphs may still point at it
-          void* fresh = nullptr;
-          if (cudaMalloc(&fresh, need) != cudaSuccess) { split = 1; }
-          else { ws = fresh; ws_bytes = need; cudaMemset(ws, 0, need); }
+          rem = 0;
+          tail_split = 1;
         }
       }
-      if (split > 1) {
+      if (rem > 0) {
         char* b = static_cast<char*>(ws);
-        p.part_o = reinterpret_cast<float*>(b);
-        p.part_ml = reinterpret_cast<float2*>(b + align_up(need_o, 256));
-        p.counters = reinterpret_cast<int*>(b + align_up(need_o, 256) + align_up(need_ml, 256));
+        p.counters = reinterpret_cast<int*>(b);
+        p.part_ml = reinterpret_cast<float2*>(b + cap_c);
+        p.part_o = reinterpret_cast<float*>(b + cap_c + cap_ml);
       }
     }
-    p.split = split;
-    const int work = items * split;
+    p.full_items = items - rem;
+    p.tail_split = tail_split;
+    const int work = p.full_items + rem * tail_split;
     const int grid2 = work < slots ? work : slots;
     if (q->d == 128) {
       cudaFuncSetAttribute(attn_fwd_v2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
