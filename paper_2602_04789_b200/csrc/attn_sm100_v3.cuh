@@ -1,0 +1,398 @@
+// K4 v3: block-sparse flash attention, one persistent CTA per SM with a
+// double-buffered S/P in TMEM.
+//
+// Contract: attention.py:168-188, 229-274 restated (see attn_sm100.cuh).
+// Structure (10 warps):
+//   warp 0      TMA producer: Q of the work unit, K_j / V_j into 2-stage rings
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer
+//   warps 2..9  softmax: warp w owns TMEM lane quarter (w & 3) = 32 query rows
+//               and column half hf = (w - 2) >> 2 of S (64 keys) and of O
+// TMEM (512 columns): S/P buffer 0 [0,128), S/P buffer 1 [128,256), O [256,256+D).
+// Issue order per work unit:  QK_0, QK_1, PV_0, QK_2, PV_1, ... , PV_last.
+// QK_{j+1} is in flight while softmax_j runs, so the softmax warps go from one
+// key tile to the next without waiting for the tensor core, and PV_j (which
+// reads P_j from TMEM, tcgen05.mma ... [a_tmem]) precedes in issue order the
+// QK_{j+2} that overwrites the same buffer.  O is rescaled lazily (row max
+// growth > 2^8), after waiting for the PV that last wrote it.
+// Work units are whole (head, query tile) items; the last partial round is
+// split over key tiles and merged by the last part to finish (as in v2).
+#pragma once
+#include "attn_sm100_v2.cuh"
+
+namespace lf {
+
+template <int D>
+struct AttnCfg3 {
+  static constexpr int BM = 128;
+  static constexpr int BN = 128;
+  static constexpr int ATOMS = D / 64;
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int SEG_BYTES = 64 * 128;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;       // 2 stages
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;  // 2 stages
+  static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024 + 1024;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int COL_S = 0;    // + 128 * buffer
+  static constexpr int COL_O = 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_constant__ AttnParams p,
+                                                              int total_work) {
+  using C = AttnCfg3<D>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sQ = smem + C::OFF_Q;
+  unsigned char* sK = smem + C::OFF_K;
+  unsigned char* sV = smem + C::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;    // [2]
+  uint64_t* k_empty = bars + 4;   // [2]
+  uint64_t* v_full = bars + 6;    // [2]
+  uint64_t* v_empty = bars + 8;   // [2]
+  uint64_t* s_full = bars + 10;   // [2]
+  uint64_t* p_full = bars + 12;   // [2]
+  uint64_t* pv_done = bars + 14;  // [2]
+  uint64_t* o_full = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(bars + 18);
+  float* red = reinterpret_cast<float*>(bars + 32);  // [2][128] row maxima / sums
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(k_full + b, 1);
+      mbar_init(k_empty + b, 1);
+      mbar_init(v_full + b, 1);
+      mbar_init(v_empty + b, 1);
+      mbar_init(s_full + b, 1);
+      mbar_init(p_full + b, 256);
+      mbar_init(pv_done + b, 1);
+    }
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      tma_prefetch(&p.tq);
+      tma_prefetch(&p.tk);
+      tma_prefetch(&p.tv);
+      uint32_t it = 0, tc = 0;
+      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        const WorkItem wi = work_item(p, w);
+        const TileCtx cx = tile_ctx(p, wi);
+        if (cx.j1 == cx.j0) continue;
+        mbar_wait(q_empty, (tc++ & 1) ^ 1);
+        mbar_expect_tx(q_full, C::Q_BYTES);
+        for (int a = 0; a < C::ATOMS; ++a)
+          tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, wi.tile * C::BM, wi.h);
+        for (int j = cx.j0; j < cx.j1; ++j, ++it) {
+          const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
+          const int st = it & 1;
+          const uint32_t par = ((it >> 1) & 1) ^ 1;
+          mbar_wait(k_empty + st, par);
+          mbar_expect_tx(k_full + st, C::KV_BYTES);
+          for (int a = 0; a < C::ATOMS; ++a) {
+            unsigned char* dst = sK + st * C::KV_BYTES + a * (C::BN * 128);
+            tma_load_3d(&p.tk, k_full + st, dst, a * 64, ts.s0, wi.h);
+            tma_load_3d(&p.tk, k_full + st, dst + C::SEG_BYTES, a * 64, ts.s1, wi.h);
+          }
+          mbar_wait(v_empty + st, par);
+          mbar_expect_tx(v_full + st, C::KV_BYTES);
+          for (int a = 0; a < C::ATOMS; ++a) {
+            unsigned char* dst = sV + st * C::KV_BYTES + a * (C::BN * 128);
+            tma_load_3d(&p.tv, v_full + st, dst, a * 64, ts.s0, wi.h);
+            tma_load_3d(&p.tv, v_full + st, dst + C::SEG_BYTES, a * 64, ts.s1, wi.h);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC_QK = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t IDESC_PV = idesc_bf16(128, D, 0, 1);
+      const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
+      auto issue_pv = [&](uint32_t i2, bool first) {
+        const int b = i2 & 1;
+        const uint32_t par = (i2 >> 1) & 1;
+        mbar_wait(p_full + b, par);
+        mbar_wait(v_full + b, par);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 16; ++kk) {
+          uint64_t bd = smem_desc_sw128(v_base + b * C::KV_BYTES + kk * 16 * 128, C::BN * 128, 1024);
+          tc_mma_ts(tmem + C::COL_O, tmem + C::COL_S + b * 128 + kk * 8, bd, IDESC_PV,
+                    (!first || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(v_empty + b);
+        tc_commit(pv_done + b);
+      };
+      uint32_t it = 0, tc = 0;
+      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        const TileCtx cx = tile_ctx(p, work_item(p, w));
+        if (cx.j1 == cx.j0) continue;
+        mbar_wait(q_full, tc++ & 1);
+        for (int j = cx.j0; j < cx.j1; ++j, ++it) {
+          const int b = it & 1;
+          mbar_wait(k_full + b, (it >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const int a = kk >> 2;
+            const uint32_t off = (kk & 3) * 32;
+            uint64_t ad = smem_desc_sw128(q_base + a * (C::BM * 128) + off, 16, 1024);
+            uint64_t bd =
+                smem_desc_sw128(k_base + b * C::KV_BYTES + a * (C::BN * 128) + off, 16, 1024);
+            tc_mma_ss(tmem + C::COL_S + b * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
+          }
+          tc_commit(k_empty + b);
+          tc_commit(s_full + b);
+          if (j == cx.j1 - 1) tc_commit(q_empty);
+          if (j > cx.j0) issue_pv(it - 1, j - 1 == cx.j0);
+        }
+        issue_pv(it - 1, cx.j1 - 1 == cx.j0);
+        tc_commit(o_full);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------- softmax + epilogue
+    const int quarter = warp & 3;
+    const int hf = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t o_col = C::COL_O + hf * (D / 2);
+    const float c2 = p.scale_log2;
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); };
+    uint32_t it = 0, tc = 0;
+    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+      const WorkItem wi = work_item(p, w);
+      const TileCtx cx = tile_ctx(p, wi);
+      const int q0 = wi.tile * C::BM;
+      const int grow = q0 + row;
+      const bool row_ok = grow < p.Lq;
+      int lq = 0;
+      if (row_ok) {
+        lq = p.qt.block_of(grow) - p.qt.block_of(q0);
+        lq = lq < 32 ? lq : 31;
+      }
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = cx.j0; j < cx.j1; ++j, ++it) {
+        const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
+        const bool full = (ts.m0 & ts.m1) == -1 && ts.l0 == 64 && ts.l1 == 64;
+        const int b = it & 1;
+        mbar_wait(s_full + b, (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t s_col = C::COL_S + b * 128 + hf * 64;
+        float v[64];
+        tmem_ld32(t_row + s_col, v);
+        tmem_ld32(t_row + s_col + 32, v + 32);
+        tmem_ld_wait();
+        if (!full) {
+          mask_chunk(v, 2 * hf, ts, lq);
+          mask_chunk(v + 32, 2 * hf + 1, ts, lq);
+        }
+        float mx[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float* u = v + 8 * g;
+          mx[g] = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
+        }
+        float mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]),
+                         fmaxf(mx[6], mx[7]));
+        red[hf * 128 + row] = mt;
+        pair_sync();
+        mt = fmaxf(mt, red[(hf ^ 1) * 128 + row]);
+        const float m_new = fmaxf(m_used, mt);
+        const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
+        const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
+        const bool rescale = __any_sync(0xffffffffu, need) && j > cx.j0;
+        if (need) {
+          l *= factor;
+          m_used = m_new;
+        }
+        const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
+        const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        // P (bf16 pairs) over this half's S columns: the partner half loaded its
+        // S before pair_sync, and P cols [b*128 + 32hf, +32) only overlap S
+        // columns of this buffer that both halves have already read
+        const uint32_t p_col = C::COL_S + b * 128 + hf * 32;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float a, bb;
+            f2unpack(ffma2(f2pack(v[32 * ch + 2 * e], v[32 * ch + 2 * e + 1]), c2v, nm), a, bb);
+            a = ex2(a);
+            bb = ex2(bb);
+            acc[e & 3] = fadd2(acc[e & 3], f2pack(a, bb));
+            pk[e] = pack_bf16(a, bb);
+          }
+          tmem_st16(t_row + p_col + 16 * ch, pk);
+        }
+        if (rescale) {
+          // O holds PV up to j-1 once that PV completes; then rescale this half
+          const uint32_t i1 = it - 1;
+          mbar_wait(pv_done + (i1 & 1), (i1 >> 1) & 1);
+          tc_fence_after();
+          float o[32];
+#pragma unroll 1
+          for (int c = 0; c < D / 64; ++c) {
+            tmem_ld32(t_row + o_col + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= factor;
+            tmem_st32(t_row + o_col + c * 32, o);
+          }
+        }
+        acc[0] = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        float a, bb;
+        f2unpack(acc[0], a, bb);
+        l += a + bb;
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(p_full + b);
+        pair_sync();  // red[] is reused by the next tile
+      }
+      if (cx.T == 0) {
+        if (row_ok && p.err) atomicOr(p.err, 1);  // no key at all (callers prevent this)
+        continue;
+      }
+      const bool empty_part = cx.j1 == cx.j0;
+      red[hf * 128 + row] = l;
+      pair_sync();
+      l += red[(hf ^ 1) * 128 + row];
+      pair_sync();
+      if (!empty_part) {
+        mbar_wait(o_full, tc++ & 1);
+        tc_fence_after();
+      }
+      if (wi.nparts > 1) {
+        // ---- split-KV: publish this part's unnormalised O, (m, l); last part merges
+        const long long unit = (long long)wi.slot * wi.nparts + wi.part;
+        float* po = p.part_o + (unit * 128 + row) * D + hf * (D / 2);
+        if (!empty_part) {
+#pragma unroll 1
+          for (int c = 0; c < D / 64; ++c) {
+            float o[32];
+            tmem_ld32(t_row + o_col + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(po + c * 32 + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          }
+        }
+        if (hf == 0) p.part_ml[unit * 128 + row] = make_float2(m_used, empty_part ? 0.f : l);
+        tc_fence_before();
+        __threadfence();
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (threadIdx.x == 64) {
+          const int old = atomicAdd(p.counters + wi.slot, 1);
+          *flag = old == wi.nparts - 1;
+          if (old == wi.nparts - 1) p.counters[wi.slot] = 0;  // reset for the next launch
+        }
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (!*flag) continue;
+        __threadfence();
+        const long long base_unit = (long long)wi.slot * wi.nparts;
+        float M = -INFINITY;
+        for (int q = 0; q < wi.nparts; ++q) M = fmaxf(M, __ldcg(&p.part_ml[(base_unit + q) * 128 + row]).x);
+        float L = 0.f, f[4];
+        for (int q = 0; q < wi.nparts; ++q) {
+          const float2 ml = __ldcg(&p.part_ml[(base_unit + q) * 128 + row]);
+          f[q] = (ml.y > 0.f && ml.x != -INFINITY) ? ex2((ml.x - M) * c2) : 0.f;
+          L += ml.y * f[q];
+        }
+        const float inv = 1.0f / L;
+        if (row_ok && hf == 0 && !(L > 0.f) && p.err) atomicOr(p.err, 1);
+        if (row_ok) {
+#pragma unroll 1
+          for (int c = 0; c < D / 2; c += 4) {
+            float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < wi.nparts; ++q) {
+              if (f[q] == 0.f) continue;
+              const float4 x = __ldcg(reinterpret_cast<const float4*>(
+                  p.part_o + ((base_unit + q) * 128 + row) * D + hf * (D / 2) + c));
+              acc4.x += x.x * f[q]; acc4.y += x.y * f[q]; acc4.z += x.z * f[q]; acc4.w += x.w * f[q];
+            }
+            const int col = hf * (D / 2) + c;
+            if (p.out_dtype == LF_F32) {
+              float* dst = reinterpret_cast<float*>(p.out) + (long long)wi.h * p.out_head_stride +
+                           (long long)grow * p.out_row_stride + col;
+              *reinterpret_cast<float4*>(dst) =
+                  make_float4(acc4.x * inv, acc4.y * inv, acc4.z * inv, acc4.w * inv);
+            } else {
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                                   (long long)wi.h * p.out_head_stride +
+                                   (long long)grow * p.out_row_stride + col;
+              *reinterpret_cast<uint2*>(dst) =
+                  make_uint2(pack_bf16(acc4.x * inv, acc4.y * inv), pack_bf16(acc4.z * inv, acc4.w * inv));
+            }
+          }
+          if (hf == 0 && p.lse)
+            p.lse[(long long)wi.h * p.Lq + grow] = (M == -INFINITY ? -INFINITY : M * p.scale) + logf(L);
+        }
+        continue;
+      }
+      // ---- epilogue: O / l -> global
+      const float inv = 1.0f / l;
+      if (row_ok && hf == 0 && !(l > 0.f) && p.err) atomicOr(p.err, 1);
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        float o[32];
+        tmem_ld32(t_row + o_col + c * 32, o);
+        tmem_ld_wait();
+        if (!row_ok) continue;
+        const int col = hf * (D / 2) + c * 32;
+        if (p.out_dtype == LF_F32) {
+          float* dst = reinterpret_cast<float*>(p.out) + (long long)wi.h * p.out_head_stride +
+                       (long long)grow * p.out_row_stride + col;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(dst + e) =
+                make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
+        } else {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                               (long long)wi.h * p.out_head_stride +
+                               (long long)grow * p.out_row_stride + col;
+#pragma unroll
+          for (int e = 0; e < 32; e += 8)
+            *reinterpret_cast<uint4*>(dst + e) = make_uint4(
+                pack_bf16(o[e] * inv, o[e + 1] * inv), pack_bf16(o[e + 2] * inv, o[e + 3] * inv),
+                pack_bf16(o[e + 4] * inv, o[e + 5] * inv), pack_bf16(o[e + 6] * inv, o[e + 7] * inv));
+        }
+      }
+      if (row_ok && hf == 0 && p.lse)
+        p.lse[(long long)wi.h * p.Lq + grow] =
+            (m_used == -INFINITY ? -INFINITY : m_used * p.scale) + logf(l);
+      tc_fence_before();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+}  // namespace lf

@@ -8,6 +8,7 @@
 
 #include "attn_sm100.cuh"
 #include "attn_sm100_v2.cuh"
+#include "attn_sm100_v3.cuh"
 #include "cag.cuh"
 #include "pool.cuh"
 #include "select.cuh"
@@ -472,8 +473,9 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (sms <= 0) sms = 148;
     }
+    static const int ver = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 3;
     const int items = p.n_qtiles * q->heads;
-    const int slots = 2 * sms;  // two co-resident CTAs per SM
+    const int slots = (ver == 2 ? 2 : 1) * sms;  // v2: two co-resident CTAs per SM
     // split-KV balancing of the last, partial round: with items = k*slots + rem,
     // the rem tail items are cut into s = slots/rem (<= 4) parts so every CTA
     // finishes at about the same time (444 items on 296 slots: 296 whole items
@@ -522,16 +524,26 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
     p.tail_split = tail_split;
     const int work = p.full_items + rem * tail_split;
     const int grid2 = work < slots ? work : slots;
-    if (q->d == 128) {
-      cudaFuncSetAttribute(attn_fwd_v2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           AttnCfg2<128>::SMEM);
-      attn_fwd_v2_kernel<128><<<grid2, 320, AttnCfg2<128>::SMEM, S(stream)>>>(p, work);
+    if (ver == 2) {
+      if (q->d == 128) {
+        cudaFuncSetAttribute(attn_fwd_v2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             AttnCfg2<128>::SMEM);
+        attn_fwd_v2_kernel<128><<<grid2, 320, AttnCfg2<128>::SMEM, S(stream)>>>(p, work);
+      } else {
+        cudaFuncSetAttribute(attn_fwd_v2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             AttnCfg2<64>::SMEM);
+        attn_fwd_v2_kernel<64><<<grid2, 320, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
+      }
+    } else if (q->d == 128) {
+      cudaFuncSetAttribute(attn_fwd_v3_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           AttnCfg3<128>::SMEM);
+      attn_fwd_v3_kernel<128><<<grid2, 320, AttnCfg3<128>::SMEM, S(stream)>>>(p, work);
     } else {
-      cudaFuncSetAttribute(attn_fwd_v2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           AttnCfg2<64>::SMEM);
-      attn_fwd_v2_kernel<64><<<grid2, 320, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
+      cudaFuncSetAttribute(attn_fwd_v3_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           AttnCfg3<64>::SMEM);
+      attn_fwd_v3_kernel<64><<<grid2, 320, AttnCfg3<64>::SMEM, S(stream)>>>(p, work);
     }
-    return check_launch("attn_fwd_v2_kernel");
+    return check_launch("attn_fwd_v2/v3_kernel");
   }
   dim3 grid(p.n_qtiles, q->heads);
   if (q->d == 128) {
