@@ -323,23 +323,51 @@ def run_ours(args, c):
     clk = clocks.stop()
     value = flops_step / (ms_step * 1e-3) / 1e12
 
-    # ---- kernel-level timing for the roofline (same kernels, same inputs, eager)
+    # ---- kernel-level timing for the roofline: the same kernels on the same
+    # inputs, each stage captured in its own CUDA graph so that no host launch
+    # gap is timed; events bracket graph replays on the current stream
     qt, kt = tilings(lay, i, True)
     bpf = lay.frame_kv_blocks
     P = (i - 1) * f
     stage = {"pool": [], "select": [], "attn": []}
+    graphs = []
+    for s in range(T):
+        st = {}
+
+        def run_pool(s=s, st=st):
+            st["views"] = D.compress(Q[s], K[s], qt, kt, bpf, P)
+
+        def run_sel(s=s, st=st):
+            qb, kb, kf = st["views"]
+            sel = D.select(qb, kb, kf, bpf, i, f, c["topk"], c["mode"] == "per-frame", s_dev)
+            st["tiles"] = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf)
+
+        def run_attn(s=s, st=st):
+            D.attention(Q[s], K[s], V[s], qt, st["tiles"], P * n, lk, out=outs[s])
+
+        fns = (run_pool, run_sel, run_attn)
+        for fn in fns:  # warm (allocates the static buffers the graphs reuse)
+            fn()
+        torch.cuda.synchronize()
+        gs = []
+        for fn in fns:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            gs.append(g)
+        graphs.append(gs)
+    torch.cuda.synchronize()
     reps = max(5, min(args.steps, 50))
     evs = []
     for r in range(reps):
         for s in range(T):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
-            qb, kb, kf = D.compress(Q[s], K[s], qt, kt, bpf, P)
+            graphs[s][0].replay()
             ev[1].record()
-            sel = D.select(qb, kb, kf, bpf, i, f, c["topk"], c["mode"] == "per-frame", s_dev)
-            tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf)
+            graphs[s][1].replay()
             ev[2].record()
-            D.attention(Q[s], K[s], V[s], qt, tiles, P * n, lk, out=outs[s])
+            graphs[s][2].replay()
             ev[3].record()
             evs.append(ev)
     torch.cuda.synchronize()

@@ -33,19 +33,24 @@ struct AttnCfg3 {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;       // 2 stages
   static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;  // 2 stages
   static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024 + 1024;
+  static constexpr int SMEM = OFF_BAR + 256 + 2048 + 1024;  // barriers, row stats, align
   static constexpr int TMEM_COLS = 512;
   static constexpr int COL_S = 0;    // + 128 * buffer
   static constexpr int COL_O = 256;
 };
 
-template <int D>
-__global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_constant__ AttnParams p,
-                                                              int total_work) {
+// CG = column groups per TMEM lane quarter: 4*CG softmax warps, each owning
+// 128/CG keys of S and D/CG columns of O for its 32 rows.
+template <int D, int CG>
+__global__ void __launch_bounds__(64 + 128 * CG, 1)
+    attn_fwd_v3_kernel(const __grid_constant__ AttnParams p, int total_work) {
   using C = AttnCfg3<D>;
+  constexpr int KW = 128 / CG;  // keys per warp
+  constexpr int DW = D / CG;    // O columns per warp
+  static_assert(KW % 32 == 0 && DW % 16 == 0, "column split");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // keep the __shared__ address space visible to the compiler (LDS/STS, not generic)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sQ = smem + C::OFF_Q;
   unsigned char* sK = smem + C::OFF_K;
   unsigned char* sV = smem + C::OFF_V;
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
   uint64_t* o_full = bars + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   uint32_t* flag = reinterpret_cast<uint32_t*>(bars + 18);
-  float* red = reinterpret_cast<float*>(bars + 32);  // [2][128] row maxima / sums
+  float* red = reinterpret_cast<float*>(bars + 32);  // [CG][128] row maxima / sums
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -76,7 +81,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
       mbar_init(v_full + b, 1);
       mbar_init(v_empty + b, 1);
       mbar_init(s_full + b, 1);
-      mbar_init(p_full + b, 256);
+      mbar_init(p_full + b, 128 * CG);
       mbar_init(pv_done + b, 1);
     }
     mbar_init(o_full, 1);
@@ -177,12 +182,26 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
   } else {
     // ------------------------------------------------------------- softmax + epilogue
     const int quarter = warp & 3;
-    const int hf = (warp - 2) >> 2;
+    const int hf = (warp - 2) >> 2;  // column group 0..CG-1
     const int row = quarter * 32 + lane;
     const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t o_col = C::COL_O + hf * (D / 2);
+    const uint32_t o_col = C::COL_O + hf * DW;
     const float c2 = p.scale_log2;
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); };
+    auto pair_sync = [&]() {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(32 * CG) : "memory");
+    };
+    auto group_other = [&](const float x, bool is_max) {
+      // combine x over the CG warps sharing this quarter (through red[])
+      red[hf * 128 + row] = x;
+      pair_sync();
+      float r = x;
+#pragma unroll
+      for (int g = 1; g < CG; ++g) {
+        const float y = red[((hf + g) % CG) * 128 + row];
+        r = is_max ? fmaxf(r, y) : r + y;
+      }
+      return r;
+    };
     uint32_t it = 0, tc = 0;
     for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
       const WorkItem wi = work_item(p, w);
@@ -202,26 +221,26 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
         const int b = it & 1;
         mbar_wait(s_full + b, (it >> 1) & 1);
         tc_fence_after();
-        const uint32_t s_col = C::COL_S + b * 128 + hf * 64;
-        float v[64];
-        tmem_ld32(t_row + s_col, v);
-        tmem_ld32(t_row + s_col + 32, v + 32);
+        const uint32_t s_col = C::COL_S + b * 128 + hf * KW;
+        float v[KW];
+#pragma unroll
+        for (int c = 0; c < KW / 32; ++c) tmem_ld32(t_row + s_col + 32 * c, v + 32 * c);
         tmem_ld_wait();
         if (!full) {
-          mask_chunk(v, 2 * hf, ts, lq);
-          mask_chunk(v + 32, 2 * hf + 1, ts, lq);
-        }
-        float mx[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
+          for (int c = 0; c < KW / 32; ++c) mask_chunk(v + 32 * c, hf * (KW / 32) + c, ts, lq);
+        }
+        float mx[KW / 8];
+#pragma unroll
+        for (int g = 0; g < KW / 8; ++g) {
           const float* u = v + 8 * g;
           mx[g] = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
         }
-        float mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]),
-                         fmaxf(mx[6], mx[7]));
-        red[hf * 128 + row] = mt;
-        pair_sync();
-        mt = fmaxf(mt, red[(hf ^ 1) * 128 + row]);
+        float mt = mx[0];
+#pragma unroll
+        for (int g = 1; g + 1 < KW / 8; g += 2) mt = fmax3(mt, mx[g], mx[g + 1]);
+        if ((KW / 8) % 2 == 0) mt = fmaxf(mt, mx[KW / 8 - 1]);
+        mt = group_other(mt, true);
         const float m_new = fmaxf(m_used, mt);
         const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
         const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
@@ -233,12 +252,12 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
         const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
         const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        // P (bf16 pairs) over this half's S columns: the partner half loaded its
-        // S before pair_sync, and P cols [b*128 + 32hf, +32) only overlap S
-        // columns of this buffer that both halves have already read
-        const uint32_t p_col = C::COL_S + b * 128 + hf * 32;
+        // P (bf16 pairs) over this group's S columns: every warp of the quarter
+        // loaded its S before the max exchange, and P cols [b*128 + hf*KW/2, +KW/2)
+        // only overlap S columns of this buffer that have already been read
+        const uint32_t p_col = C::COL_S + b * 128 + hf * (KW / 2);
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+        for (int ch = 0; ch < KW / 32; ++ch) {
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -256,14 +275,14 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
           const uint32_t i1 = it - 1;
           mbar_wait(pv_done + (i1 & 1), (i1 >> 1) & 1);
           tc_fence_after();
-          float o[32];
+          float o[16];
 #pragma unroll 1
-          for (int c = 0; c < D / 64; ++c) {
-            tmem_ld32(t_row + o_col + c * 32, o);
+          for (int c = 0; c < DW / 16; ++c) {
+            tmem_ld16(t_row + o_col + c * 16, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= factor;
-            tmem_st32(t_row + o_col + c * 32, o);
+            for (int e = 0; e < 16; ++e) o[e] *= factor;
+            tmem_st16(t_row + o_col + c * 16, reinterpret_cast<uint32_t*>(o));
           }
         }
         acc[0] = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
@@ -280,9 +299,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
         continue;
       }
       const bool empty_part = cx.j1 == cx.j0;
-      red[hf * 128 + row] = l;
-      pair_sync();
-      l += red[(hf ^ 1) * 128 + row];
+      l = group_other(l, false);
       pair_sync();
       if (!empty_part) {
         mbar_wait(o_full, tc++ & 1);
@@ -291,28 +308,28 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
       if (wi.nparts > 1) {
         // ---- split-KV: publish this part's unnormalised O, (m, l); last part merges
         const long long unit = (long long)wi.slot * wi.nparts + wi.part;
-        float* po = p.part_o + (unit * 128 + row) * D + hf * (D / 2);
+        float* po = p.part_o + (unit * 128 + row) * D + hf * DW;
         if (!empty_part) {
 #pragma unroll 1
-          for (int c = 0; c < D / 64; ++c) {
-            float o[32];
-            tmem_ld32(t_row + o_col + c * 32, o);
+          for (int c = 0; c < DW / 16; ++c) {
+            float o[16];
+            tmem_ld16(t_row + o_col + c * 16, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; e += 4)
-              *reinterpret_cast<float4*>(po + c * 32 + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+            for (int e = 0; e < 16; e += 4)
+              *reinterpret_cast<float4*>(po + c * 16 + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
           }
         }
         if (hf == 0) p.part_ml[unit * 128 + row] = make_float2(m_used, empty_part ? 0.f : l);
         tc_fence_before();
         __threadfence();
-        asm volatile("bar.sync 5, 256;" ::: "memory");
+        asm volatile("bar.sync 5, %0;" ::"r"(128 * CG) : "memory");
         if (threadIdx.x == 64) {
           const int old = atomicAdd(p.counters + wi.slot, 1);
           *flag = old == wi.nparts - 1;
           if (old == wi.nparts - 1) p.counters[wi.slot] = 0;  // reset for the next launch
         }
-        asm volatile("bar.sync 5, 256;" ::: "memory");
+        asm volatile("bar.sync 5, %0;" ::"r"(128 * CG) : "memory");
         if (!*flag) continue;
         __threadfence();
         const long long base_unit = (long long)wi.slot * wi.nparts;
@@ -328,15 +345,15 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
         if (row_ok && hf == 0 && !(L > 0.f) && p.err) atomicOr(p.err, 1);
         if (row_ok) {
 #pragma unroll 1
-          for (int c = 0; c < D / 2; c += 4) {
+          for (int c = 0; c < DW; c += 4) {
             float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int q = 0; q < wi.nparts; ++q) {
               if (f[q] == 0.f) continue;
               const float4 x = __ldcg(reinterpret_cast<const float4*>(
-                  p.part_o + ((base_unit + q) * 128 + row) * D + hf * (D / 2) + c));
+                  p.part_o + ((base_unit + q) * 128 + row) * D + hf * DW + c));
               acc4.x += x.x * f[q]; acc4.y += x.y * f[q]; acc4.z += x.z * f[q]; acc4.w += x.w * f[q];
             }
-            const int col = hf * (D / 2) + c;
+            const int col = hf * DW + c;
             if (p.out_dtype == LF_F32) {
               float* dst = reinterpret_cast<float*>(p.out) + (long long)wi.h * p.out_head_stride +
                            (long long)grow * p.out_row_stride + col;
@@ -359,17 +376,17 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
       const float inv = 1.0f / l;
       if (row_ok && hf == 0 && !(l > 0.f) && p.err) atomicOr(p.err, 1);
 #pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        float o[32];
-        tmem_ld32(t_row + o_col + c * 32, o);
+      for (int c = 0; c < DW / 16; ++c) {
+        float o[16];
+        tmem_ld16(t_row + o_col + c * 16, o);
         tmem_ld_wait();
         if (!row_ok) continue;
-        const int col = hf * (D / 2) + c * 32;
+        const int col = hf * DW + c * 16;
         if (p.out_dtype == LF_F32) {
           float* dst = reinterpret_cast<float*>(p.out) + (long long)wi.h * p.out_head_stride +
                        (long long)grow * p.out_row_stride + col;
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
+          for (int e = 0; e < 16; e += 4)
             *reinterpret_cast<float4*>(dst + e) =
                 make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
         } else {
@@ -377,7 +394,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd_v3_kernel(const __grid_consta
                                (long long)wi.h * p.out_head_stride +
                                (long long)grow * p.out_row_stride + col;
 #pragma unroll
-          for (int e = 0; e < 32; e += 8)
+          for (int e = 0; e < 16; e += 8)
             *reinterpret_cast<uint4*>(dst + e) = make_uint4(
                 pack_bf16(o[e] * inv, o[e + 1] * inv), pack_bf16(o[e + 2] * inv, o[e + 3] * inv),
                 pack_bf16(o[e + 4] * inv, o[e + 5] * inv), pack_bf16(o[e + 6] * inv, o[e + 7] * inv));

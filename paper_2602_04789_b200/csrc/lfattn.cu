@@ -534,14 +534,16 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
                              AttnCfg2<64>::SMEM);
         attn_fwd_v2_kernel<64><<<grid2, 320, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
       }
-    } else if (q->d == 128) {
-      cudaFuncSetAttribute(attn_fwd_v3_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           AttnCfg3<128>::SMEM);
-      attn_fwd_v3_kernel<128><<<grid2, 320, AttnCfg3<128>::SMEM, S(stream)>>>(p, work);
     } else {
-      cudaFuncSetAttribute(attn_fwd_v3_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           AttnCfg3<64>::SMEM);
-      attn_fwd_v3_kernel<64><<<grid2, 320, AttnCfg3<64>::SMEM, S(stream)>>>(p, work);
+      static const int cg = getenv("LF_ATTN_CG") ? atoi(getenv("LF_ATTN_CG")) : 4;
+#define LF_V3(DD, CGV)                                                                          \
+  if (q->d == DD && cg == CGV) {                                                                \
+    cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, CGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         AttnCfg3<DD>::SMEM);                                                   \
+    attn_fwd_v3_kernel<DD, CGV><<<grid2, 64 + 128 * CGV, AttnCfg3<DD>::SMEM, S(stream)>>>(p, work); \
+  }
+      LF_V3(128, 4) LF_V3(128, 2) LF_V3(64, 4) LF_V3(64, 2)
+#undef LF_V3
     }
     return check_launch("attn_fwd_v2/v3_kernel");
   }
