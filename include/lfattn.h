@@ -95,6 +95,17 @@ int lf_select(const float* q_block, const float* k_block, const float* k_frame, 
               int32_t* out_count, int32_t* out_frames, double* out_scores, double* out_fscores,
               int32_t* out_budget, void* stream);
 
+/* lf_select with explicit per-head strides (elements) of k_block / k_frame, so
+ * the selection can read a capacity-sized summary cache (incremental rollout,
+ * see paper_2602_04789_b200/rollout.py).  Same semantics as lf_select. */
+int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_head_stride,
+                      const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
+                      int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+                      int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+                      const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+                      int32_t* out_count, int32_t* out_frames, double* out_scores,
+                      double* out_fscores, int32_t* out_budget, void* stream);
+
 /* Chunk-Aware Growth plan on device (planner.py:126-175, _solve_clamped
  * 178-208, alpha_schedule 56-66, s_max_for_chunk 113-116, chunk_block_budget
  * 119-123).  Outputs (device): alpha[N], s[N], budgets[N], clamped[N],

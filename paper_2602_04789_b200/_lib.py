@@ -25,6 +25,7 @@ LF_F32, LF_BF16 = 0, 1
 # every symbol include/lfattn.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "lf_version", "lf_strerror", "lf_last_error", "lf_pool_blocks", "lf_compress", "lf_select",
+    "lf_select_strided",
     "lf_cag_plan", "lf_plan_tiles", "lf_attention", "lf_hsa_workspace_bytes", "lf_hsa_views",
     "lf_hsa_forward", "lf_rowdot", "lf_topk",
 )
@@ -62,6 +63,8 @@ _SIGS = {
                      _P, _P, _P], ctypes.c_int),
     "lf_select": ([_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P,
                    _P, _P], ctypes.c_int),
+    "lf_select_strided": ([_P, _P, ctypes.c_int64, _P, ctypes.c_int64, _I, _I, _I, _I, _I, _I, _I,
+                           _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "lf_cag_plan": ([ctypes.c_double, ctypes.c_double, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P,
                      _P, _P, _P, _P], ctypes.c_int),
     "lf_plan_tiles": ([_P, _P, _I, _I, _I, LfTiling, LfTiling, _I, _I, _P, _P, _P], ctypes.c_int),

@@ -9,6 +9,7 @@
 #include "attn_sm100.cuh"
 #include "attn_sm100_v2.cuh"
 #include "attn_sm100_v3.cuh"
+#include "attn_sm100_v4.cuh"
 #include "cag.cuh"
 #include "pool.cuh"
 #include "select.cuh"
@@ -345,12 +346,13 @@ static int select_smem_per_warp(int d, int P, int frame_cap, int max_cand) {
   return (int)align_up(b, 16);
 }
 
-int lf_select(const float* q_block, const float* k_block, const float* k_frame, int32_t heads,
-              int32_t nqb, int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
-              int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
-              const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
-              int32_t* out_count, int32_t* out_frames, double* out_scores, double* out_fscores,
-              int32_t* out_budget, void* stream) {
+int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_head_stride,
+                      const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
+                      int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+                      int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+                      const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+                      int32_t* out_count, int32_t* out_frames, double* out_scores,
+                      double* out_fscores, int32_t* out_budget, void* stream) {
   if (!q_block || !k_block || !s_i_dev || !out_blocks || !out_count || !out_frames)
     return fail(LF_ERR_INVALID, "lf_select: null pointer");
   if (heads < 1 || nqb < 1 || d < 1 || blocks_per_frame < 1 || chunk_index < 1 || frames_per_chunk < 1)
@@ -368,13 +370,26 @@ int lf_select(const float* q_block, const float* k_block, const float* k_frame, 
   SelArgs a{q_block, k_block, k_frame, heads, nqb, nkb, d, blocks_per_frame, chunk_index,
             frames_per_chunk, topk_frames, per_frame_mode ? 1 : 0, s_i_dev, cap, frame_cap,
             out_blocks, out_count, out_frames, out_scores, out_fscores, out_budget, wpc, spw,
-            max_cand};
+            max_cand, (long long)kb_head_stride, (long long)kf_head_stride};
   const int smem = wpc * spw;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int warps = heads * nqb;
   select_kernel<<<(warps + wpc - 1) / wpc, 32 * wpc, smem, S(stream)>>>(a);
   return check_launch("select_kernel");
+}
+
+int lf_select(const float* q_block, const float* k_block, const float* k_frame, int32_t heads,
+              int32_t nqb, int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+              int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+              const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+              int32_t* out_count, int32_t* out_frames, double* out_scores, double* out_fscores,
+              int32_t* out_budget, void* stream) {
+  const int64_t P = (int64_t)(chunk_index - 1) * frames_per_chunk;
+  return lf_select_strided(q_block, k_block, (int64_t)nkb * d, k_frame, P * d, heads, nqb, nkb, d,
+                           blocks_per_frame, chunk_index, frames_per_chunk, topk_frames,
+                           per_frame_mode, s_i_dev, cap, frame_cap, out_blocks, out_count,
+                           out_frames, out_scores, out_fscores, out_budget, stream);
 }
 
 int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f, int32_t n,
@@ -473,7 +488,7 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (sms <= 0) sms = 148;
     }
-    static const int ver = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 3;
+    static const int ver = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 4;
     const int items = p.n_qtiles * q->heads;
     const int slots = (ver == 2 ? 2 : 1) * sms;  // v2: two co-resident CTAs per SM
     // split-KV balancing of the last, partial round: with items = k*slots + rem,
@@ -534,8 +549,18 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
                              AttnCfg2<64>::SMEM);
         attn_fwd_v2_kernel<64><<<grid2, 320, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
       }
+    } else if (ver == 4) {
+      if (q->d == 128) {
+        cudaFuncSetAttribute(attn_fwd_v4_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             AttnCfg4<128>::SMEM);
+        attn_fwd_v4_kernel<128><<<grid2, 576, AttnCfg4<128>::SMEM, S(stream)>>>(p, work);
+      } else {
+        cudaFuncSetAttribute(attn_fwd_v4_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             AttnCfg4<64>::SMEM);
+        attn_fwd_v4_kernel<64><<<grid2, 576, AttnCfg4<64>::SMEM, S(stream)>>>(p, work);
+      }
     } else {
-      static const int cg = getenv("LF_ATTN_CG") ? atoi(getenv("LF_ATTN_CG")) : 4;
+      static const int cg = getenv("LF_ATTN_CG") ? atoi(getenv("LF_ATTN_CG")) : 2;
 #define LF_V3(DD, CGV)                                                                          \
   if (q->d == DD && cg == CGV) {                                                                \
     cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, CGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \

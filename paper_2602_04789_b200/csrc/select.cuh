@@ -34,6 +34,7 @@ struct SelArgs {
   int warps_per_cta;
   int smem_per_warp;  // bytes
   int max_cand;
+  long long kb_head_stride, kf_head_stride;  // elements (k_block / k_frame per head)
 };
 
 __device__ __forceinline__ double dot_f32_dd(const float* __restrict__ row, const float* qv, int d) {
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(128) select_kernel(SelArgs a) {
   __syncwarp();
 
   // frame scores
-  const float* kf = a.k_frame + (size_t)h * P * a.d;
+  const float* kf = a.k_frame + (size_t)h * a.kf_head_stride;
   for (int t = lane; t < P; t += 32) fsc[t] = dot_f32_dd(kf + (size_t)t * a.d, qv, a.d);
   __syncwarp();
   if (a.out_fscores) {
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(128) select_kernel(SelArgs a) {
   }
 
   // candidate scores, ascending (frame, block)
-  const float* kb = a.k_block + (size_t)h * a.nkb * a.d;
+  const float* kb = a.k_block + (size_t)h * a.kb_head_stride;
   for (int c = lane; c < C; c += 32) {
     int t = fsel[c / bpf];
     int blk = t * bpf + (c - (c / bpf) * bpf);

@@ -103,7 +103,11 @@ class Selections:
 
 def select(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: int, per_frame: bool,
            s_i, want_scores: bool = False) -> Selections:
-    """Frame top-k + block top-budget for every (head, query block)."""
+    """Frame top-k + block top-budget for every (head, query block).
+
+    k_block / k_frame may be capacity-sized caches [H, cap, d] (only the
+    first past blocks / frames are read); their head strides are passed on.
+    """
     lib = L.lib()
     H, nqb, d = q_block.shape
     nkb = k_block.shape[1]
@@ -120,11 +124,15 @@ def select(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: int, p
     budget = torch.zeros(4, dtype=torch.int32, device=dev)
     scores = torch.empty((H, nqb, cap), dtype=torch.float64, device=dev) if want_scores else None
     fscores = torch.empty((H, nqb, max(P, 1)), dtype=torch.float64, device=dev) if want_scores else None
-    L.check(lib.lf_select(q_block.data_ptr(), k_block.data_ptr(),
-                          k_frame.data_ptr() if P > 0 else None, H, nqb, nkb, d, int(bpf),
-                          int(chunk), int(f), int(topk), 1 if per_frame else 0, s_i.data_ptr(),
-                          cap, frame_cap, blocks.data_ptr(), count.data_ptr(), frames.data_ptr(),
-                          L.ptr(scores), L.ptr(fscores), budget.data_ptr(), L.stream_ptr()))
+    for t in (q_block, k_block, k_frame):
+        assert t.stride(2) == 1 and t.stride(1) == d, "summaries must have contiguous rows"
+    L.check(lib.lf_select_strided(q_block.data_ptr(), k_block.data_ptr(), k_block.stride(0),
+                                  k_frame.data_ptr() if P > 0 else None,
+                                  k_frame.stride(0) if P > 0 else 0, H, nqb, nkb, d, int(bpf),
+                                  int(chunk), int(f), int(topk), 1 if per_frame else 0,
+                                  s_i.data_ptr(), cap, frame_cap, blocks.data_ptr(),
+                                  count.data_ptr(), frames.data_ptr(), L.ptr(scores),
+                                  L.ptr(fscores), budget.data_ptr(), L.stream_ptr()))
     return Selections(blocks, count, frames, budget, scores, fscores)
 
 

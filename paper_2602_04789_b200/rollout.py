@@ -1,0 +1,132 @@
+"""Device-resident rollout driver with an incremental pooled-summary cache.
+
+The reference's rollout (rollout.py:276-309) calls ``HsaBackend.run`` ->
+``hsa_attention`` on every denoising step with the full concatenated K/V
+(rollout.py:263-266), and ``compress`` re-pools the whole key context each
+time (selection.py:109-111), although past chunks are fixed once committed
+(rollout.py:306-308).  ``HsaRollout`` keeps the KV cache on the GPU and pools
+each clean chunk's key blocks and frame summaries exactly once, when the
+chunk is committed; a denoising step then pools only its query chunk:
+selection reads past summaries from the cache.
+
+Selections and outputs are bit-identical to ``HsaPipeline`` on the same
+inputs: the selection only ever reads *past* block/frame summaries, and those
+come from the same pooling kernels applied to the same rows (the current
+chunk's key summaries are never candidates, selection.py:137-175).
+
+Per step: pool Q (1 launch) -> select -> plan tiles -> attention (4 launches),
+HBM traffic for pooling f*n*d*2 bytes per head instead of (i+1)*f*n*d*2.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import device as D
+from .layout import ChunkLayout
+from .planner import SparsityPlan
+from .selection import SelectionConfig, tilings
+
+
+class HsaRollout:
+    def __init__(self, layout: ChunkLayout, heads: int, plan: SparsityPlan | None = None,
+                 cfg: SelectionConfig | None = None, framewise: bool | None = None,
+                 out_dtype=torch.bfloat16, device=None):
+        self.layout = layout
+        self.heads = int(heads)
+        self.plan = plan
+        self.cfg = cfg or SelectionConfig()
+        self.framewise = (not layout.aligned) if framewise is None else bool(framewise)
+        if not self.framewise and not layout.aligned:
+            raise ValueError(
+                f"selection needs b_q and b_kv to divide n: n={layout.n}, b_q={layout.b_q}, "
+                f"b_kv={layout.b_kv}")
+        self.out_dtype = out_dtype
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        lay = layout
+        H, d = self.heads, lay.d
+        self.bpf = lay.frame_kv_blocks
+        self.cap_tokens = lay.N * lay.f * lay.n
+        # device KV cache and summary caches, sized for the whole rollout
+        self.kv_k = torch.zeros((H, self.cap_tokens, d), dtype=torch.bfloat16, device=self.device)
+        self.kv_v = torch.zeros((H, self.cap_tokens, d), dtype=torch.bfloat16, device=self.device)
+        self.kb_cache = torch.zeros((H, lay.N * lay.f * self.bpf, d), dtype=torch.float32,
+                                    device=self.device)
+        self.kf_cache = torch.zeros((H, lay.N * lay.f, d), dtype=torch.float32, device=self.device)
+        self.committed = 0  # chunks whose clean K/V are in the cache
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    # ------------------------------------------------------------------ helpers
+    def _slot(self, i: int) -> slice:
+        cl = self.layout.chunk_tokens
+        return slice((i - 1) * cl, i * cl)
+
+    def _s_dev(self, i: int, s_i):
+        if s_i is not None:
+            if torch.is_tensor(s_i):
+                return s_i
+            return torch.tensor([float(s_i)], dtype=torch.float64, device=self.device)
+        if self.plan is None:
+            raise ValueError("no sparsity plan: pass s_i")
+        return self.plan.s_device(i)
+
+    # ------------------------------------------------------------------ API
+    def commit(self, k_clean: torch.Tensor, v_clean: torch.Tensor, chunk_index: int) -> None:
+        """Append chunk i's clean K/V (rollout.py:306-308) and pool its summaries once."""
+        lay = self.layout
+        i = int(chunk_index)
+        if i != self.committed + 1:
+            raise ValueError(f"chunks must be committed in order: expected {self.committed + 1}, got {i}")
+        lay.check_chunk(i)
+        sl = self._slot(i)
+        self.kv_k[:, sl].copy_(k_clean)
+        self.kv_v[:, sl].copy_(v_clean)
+        # k_block rows of this chunk's frames
+        spec = D.TilingSpec(lay.chunk_tokens, lay.n if self.framewise else lay.chunk_tokens,
+                            lay.b_kv)
+        nb = lay.f * self.bpf
+        kb = self.kb_cache[:, (i - 1) * nb:i * nb]
+        self._pool_into(self.kv_k[:, sl], spec, kb)
+        # k_frame rows = mean of each frame's block means (selection.py:111)
+        fspec = D.TilingSpec(nb, nb, self.bpf)
+        self._pool_into(kb, fspec, self.kf_cache[:, (i - 1) * lay.f:i * lay.f])
+        self.committed = i
+
+    def _pool_into(self, x: torch.Tensor, spec: D.TilingSpec, out: torch.Tensor) -> None:
+        import ctypes
+
+        from . import _lib as L
+        lib = L.lib()
+        m = L.mat(x)
+        L.check(lib.lf_pool_blocks(ctypes.byref(m), spec.abi(), -1, out.data_ptr(), out.stride(0),
+                                   L.stream_ptr()))
+
+    def step(self, q: torch.Tensor, k_cur: torch.Tensor, v_cur: torch.Tensor, chunk_index: int,
+             s_i=None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """One denoising step of chunk i (rollout.py:254-273 attention part).
+
+        q, k_cur, v_cur: bf16 [H, f*n, d] for the noisy current chunk.
+        Past chunks 1..i-1 must have been committed.
+        """
+        lay = self.layout
+        i = int(chunk_index)
+        lay.check_chunk(i)
+        if self.committed != i - 1:
+            raise ValueError(f"chunk {i} needs chunks 1..{i - 1} committed (have {self.committed})")
+        sl = self._slot(i)
+        self.kv_k[:, sl].copy_(k_cur)
+        self.kv_v[:, sl].copy_(v_cur)
+        qt, kt = tilings(lay, i, self.framewise)
+        P = (i - 1) * lay.f
+        q_block = D.pool_blocks(q, qt)
+        s_dev = self._s_dev(i, s_i)
+        sel = D.select(q_block, self.kb_cache, self.kf_cache, self.bpf, i, lay.f,
+                       self.cfg.topk_frames, self.cfg.block_budget_mode == "per-frame", s_dev)
+        tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * self.bpf)
+        lk = lay.context_tokens(i)
+        self.last_selection = sel
+        return D.attention(q, self.kv_k[:, :lk], self.kv_v[:, :lk], qt, tiles, P * lay.n, lk,
+                           out=out, out_dtype=self.out_dtype, scale=1.0 / math.sqrt(lay.d),
+                           err=self.err)
