@@ -66,7 +66,7 @@ __device__ __forceinline__ void store_row(const AttnParams& p, int h, int grow, 
 }
 
 template <int D>
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(104)
     attn_fwd_v4_kernel(const __grid_constant__ AttnParams p, int total_work) {
   using C = AttnCfg4<D>;
   constexpr int DQ = D / 4;  // output columns per softmax warp in the epilogue

@@ -73,11 +73,18 @@ class HsaRollout:
         return self.plan.s_device(i)
 
     # ------------------------------------------------------------------ API
-    def commit(self, k_clean: torch.Tensor, v_clean: torch.Tensor, chunk_index: int) -> None:
-        """Append chunk i's clean K/V (rollout.py:306-308) and pool its summaries once."""
+    def commit(self, k_clean: torch.Tensor, v_clean: torch.Tensor, chunk_index: int,
+               overwrite: bool = False) -> None:
+        """Append chunk i's clean K/V (rollout.py:306-308) and pool its summaries once.
+
+        ``overwrite`` re-writes an already committed chunk in place (used by
+        the benchmark to replay one chunk of a steady-state rollout).
+        """
         lay = self.layout
         i = int(chunk_index)
-        if i != self.committed + 1:
+        if overwrite and 1 <= i <= self.committed:
+            pass
+        elif i != self.committed + 1:
             raise ValueError(f"chunks must be committed in order: expected {self.committed + 1}, got {i}")
         lay.check_chunk(i)
         sl = self._slot(i)
@@ -92,7 +99,23 @@ class HsaRollout:
         # k_frame rows = mean of each frame's block means (selection.py:111)
         fspec = D.TilingSpec(nb, nb, self.bpf)
         self._pool_into(kb, fspec, self.kf_cache[:, (i - 1) * lay.f:i * lay.f])
-        self.committed = i
+        self.committed = max(self.committed, i)
+
+    def selection_flops(self) -> int:
+        """Exact-extent FLOPs (4*rows*cols*d over active tiles) of the last step."""
+        import numpy as np
+        sel, i = self.last_selection, self.last_chunk
+        qt, kt = tilings(self.layout, i, self.framewise)
+        b, c = sel.blocks.cpu().numpy(), sel.count.cpu().numpy()
+        qb, kb = qt.bounds(), kt.bounds()
+        rows = (qb[:, 1] - qb[:, 0]).astype(np.int64)
+        cols = (kb[:, 1] - kb[:, 0]).astype(np.int64)
+        cur = int(cols[(i - 1) * self.layout.f * self.bpf:].sum())
+        total = 0
+        for h in range(self.heads):
+            for r in range(qt.count):
+                total += int(rows[r]) * (cur + int(cols[b[h, r, :c[h, r]]].sum()))
+        return int(4 * self.layout.d * total)
 
     def _pool_into(self, x: torch.Tensor, spec: D.TilingSpec, out: torch.Tensor) -> None:
         import ctypes
@@ -127,6 +150,7 @@ class HsaRollout:
         tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * self.bpf)
         lk = lay.context_tokens(i)
         self.last_selection = sel
+        self.last_chunk = i
         return D.attention(q, self.kv_k[:, :lk], self.kv_v[:, :lk], qt, tiles, P * lay.n, lk,
                            out=out, out_dtype=self.out_dtype, scale=1.0 / math.sqrt(lay.d),
                            err=self.err)
