@@ -550,15 +550,23 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
         attn_fwd_v2_kernel<64><<<grid2, 320, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
       }
     } else if (ver == 4) {
-      if (q->d == 128) {
-        cudaFuncSetAttribute(attn_fwd_v4_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             AttnCfg4<128>::SMEM);
-        attn_fwd_v4_kernel<128><<<grid2, 576, AttnCfg4<128>::SMEM, S(stream)>>>(p, work);
-      } else {
-        cudaFuncSetAttribute(attn_fwd_v4_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             AttnCfg4<64>::SMEM);
-        attn_fwd_v4_kernel<64><<<grid2, 576, AttnCfg4<64>::SMEM, S(stream)>>>(p, work);
+      const void* fn = q->d == 128 ? (const void*)attn_fwd_v4_kernel<128>
+                                   : (const void*)attn_fwd_v4_kernel<64>;
+      const int smem = q->d == 128 ? AttnCfg4<128>::SMEM : AttnCfg4<64>::SMEM;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (q->d == 128)
+        attn_fwd_v4_kernel<128><<<grid2, 576, smem, S(stream)>>>(p, work);
+      else
+        attn_fwd_v4_kernel<64><<<grid2, 576, smem, S(stream)>>>(p, work);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, fn);
+        return fail(LF_ERR_CUDA, "attn_fwd_v4_kernel: %s (regs %d, max threads %d, dyn smem %d/%d)",
+                    cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, smem,
+                    fa.maxDynamicSharedSizeBytes);
       }
+      return LF_OK;
     } else {
       static const int cg = getenv("LF_ATTN_CG") ? atoi(getenv("LF_ATTN_CG")) : 2;
 #define LF_V3(DD, CGV)                                                                          \
