@@ -66,7 +66,9 @@ __device__ __forceinline__ void store_row(const AttnParams& p, int h, int grow, 
 }
 
 template <int D>
-__global__ void __maxnreg__(104)
+// 18 warps: the register file is split per SM sub-partition (16K each), and one
+// sub-partition holds 5 warps -> at most 102 registers per thread (96 allocated)
+__global__ void __maxnreg__(96)
     attn_fwd_v4_kernel(const __grid_constant__ AttnParams p, int total_work) {
   using C = AttnCfg4<D>;
   constexpr int DQ = D / 4;  // output columns per softmax warp in the epilogue
@@ -168,7 +170,9 @@ __global__ void __maxnreg__(104)
 #pragma unroll
         for (int kk = 0; kk < C::BN / 16; ++kk) {
           uint64_t bd = smem_desc_sw128(v_base + st * C::KV_BYTES + kk * 16 * 128, C::BN * 128, 1024);
-          tc_mma_ts(tmem + C::COL_O + X * 128, tmem + C::COL_S + X * 128 + kk * 8, bd, IDESC_PV,
+          // P of keys 0..63 at columns 0..31, of keys 64..127 at columns 64..95
+          tc_mma_ts(tmem + C::COL_O + X * 128,
+                    tmem + C::COL_S + X * 128 + kk * 8 + (kk >= 4 ? 32 : 0), bd, IDESC_PV,
                     (!first || kk > 0) ? 1u : 0u);
         }
         tc_commit(v_empty + st);
@@ -241,23 +245,24 @@ __global__ void __maxnreg__(104)
         const bool full = (ts.m0 & ts.m1) == -1 && ts.l0 == 64 && ts.l1 == 64;
         mbar_wait(s_full + X, itx & 1);
         tc_fence_after();
+        // two passes over this half's 64 S columns in 32-column chunks (max, then
+        // exp) keep the register footprint of 18 warps under the 96-register cap
         const uint32_t s_col = C::COL_S + X * 128 + hf * 64;
-        float v[64];
-        tmem_ld32(t_row + s_col, v);
-        tmem_ld32(t_row + s_col + 32, v + 32);
-        tmem_ld_wait();
-        if (!full) {
-          mask_chunk(v, 2 * hf, ts, lq);
-          mask_chunk(v + 32, 2 * hf + 1, ts, lq);
-        }
-        float mx[8];
+        float mt = -INFINITY;
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const float* u = v + 8 * g;
-          mx[g] = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
+        for (int ch = 0; ch < 2; ++ch) {
+          float v[32];
+          tmem_ld32(t_row + s_col + 32 * ch, v);
+          tmem_ld_wait();
+          if (!full) mask_chunk(v, 2 * hf + ch, ts, lq);
+          float mx[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float* u = v + 8 * g;
+            mx[g] = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
+          }
+          mt = fmax3(mt, fmax3(mx[0], mx[1], mx[2]), mx[3]);
         }
-        float mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]),
-                         fmaxf(mx[6], mx[7]));
         my_red[hf * 128 + row] = mt;
         pair_sync();
         mt = fmaxf(mt, my_red[(hf ^ 1) * 128 + row]);
@@ -272,15 +277,22 @@ __global__ void __maxnreg__(104)
         const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
         const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        // P over this half's S columns (both halves loaded S before pair_sync)
-        const uint32_t p_col = C::COL_S + X * 128 + hf * 32;
+        // P (bf16 pairs) of this half goes to TMEM columns [X*128 + 64hf, +32),
+        // i.e. over this half's own first S chunk, which is already consumed;
+        // the PV MMA reads keys 0..63 from columns 0..31 and keys 64..127 from
+        // columns 64..95 of the buffer
+        const uint32_t p_col = C::COL_S + X * 128 + hf * 64;
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
+          float v[32];
+          tmem_ld32(t_row + s_col + 32 * ch, v);
+          tmem_ld_wait();
+          if (!full) mask_chunk(v, 2 * hf + ch, ts, lq);
           uint32_t pkv[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             float a, bb;
-            f2unpack(ffma2(f2pack(v[32 * ch + 2 * e], v[32 * ch + 2 * e + 1]), c2v, nm), a, bb);
+            f2unpack(ffma2(f2pack(v[2 * e], v[2 * e + 1]), c2v, nm), a, bb);
             a = ex2(a);
             bb = ex2(bb);
             acc[e & 3] = fadd2(acc[e & 3], f2pack(a, bb));
@@ -332,11 +344,13 @@ __global__ void __maxnreg__(104)
         mbar_wait(o_full, tc++ & 1);
         tc_fence_after();
       }
-      // this warp's output columns: [cw, cw + D/4)
+      // this warp's output columns [cw, cw + D/4), 16 at a time
       const int cw = (X * 2 + hf) * DQ;
-      float ov[DQ];
+      const long long unit = (long long)wi.slot * wi.nparts + wi.part;
+      if (wi.nparts == 1 && row_ok && X == 0 && hf == 0 && !(L > 0.f) && p.err) atomicOr(p.err, 1);
       if (!empty_part) {
-#pragma unroll
+        const float inv = 1.0f / L;
+#pragma unroll 1
         for (int c = 0; c < DQ / 16; ++c) {
           float oa[16], ob[16];
           tmem_ld16(t_row + C::COL_O + cw + c * 16, oa);
@@ -344,20 +358,23 @@ __global__ void __maxnreg__(104)
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            ov[c * 16 + e] = (fa != 0.f ? oa[e] * fa : 0.f) + (fb != 0.f ? ob[e] * fb : 0.f);
+            oa[e] = (fa != 0.f ? oa[e] * fa : 0.f) + (fb != 0.f ? ob[e] * fb : 0.f);
+          if (wi.nparts == 1) {
+            if (row_ok) store_row<D, 16>(p, wi.h, grow, cw + c * 16, oa, inv);
+          } else {
+            float* po = p.part_o + (unit * 128 + row) * D + cw + c * 16;
+#pragma unroll
+            for (int e = 0; e < 16; e += 4)
+              *reinterpret_cast<float4*>(po + e) = make_float4(oa[e], oa[e + 1], oa[e + 2], oa[e + 3]);
+          }
         }
       }
+      if (wi.nparts == 1 && row_ok && X == 0 && hf == 0 && p.lse)
+        p.lse[(long long)wi.h * p.Lq + grow] = (M == -INFINITY ? -INFINITY : M * p.scale) + logf(L);
       tc_fence_before();
       all_sync();  // every warp has read O_A/O_B and stat[] before they are reused
       if (wi.nparts > 1) {
-        // ---- split-KV tail: publish (O, M, L) of this part; the last part merges
-        const long long unit = (long long)wi.slot * wi.nparts + wi.part;
-        float* po = p.part_o + (unit * 128 + row) * D + cw;
-        if (!empty_part) {
-#pragma unroll
-          for (int e = 0; e < DQ; e += 4)
-            *reinterpret_cast<float4*>(po + e) = make_float4(ov[e], ov[e + 1], ov[e + 2], ov[e + 3]);
-        }
+        // ---- split-KV tail: publish (M, L) of this part; the last part merges
         if (X == 0 && hf == 0)
           p.part_ml[unit * 128 + row] = make_float2(M, empty_part ? 0.f : L);
         __threadfence();
@@ -374,7 +391,8 @@ __global__ void __maxnreg__(104)
         __threadfence();
         const long long base_unit = (long long)wi.slot * wi.nparts;
         float MM = -INFINITY;
-        for (int q = 0; q < wi.nparts; ++q) MM = fmaxf(MM, __ldcg(&p.part_ml[(base_unit + q) * 128 + row]).x);
+        for (int q = 0; q < wi.nparts; ++q)
+          MM = fmaxf(MM, __ldcg(&p.part_ml[(base_unit + q) * 128 + row]).x);
         float LL = 0.f, f[4];
         for (int q = 0; q < wi.nparts; ++q) {
           const float2 ml = __ldcg(&p.part_ml[(base_unit + q) * 128 + row]);
@@ -382,30 +400,25 @@ __global__ void __maxnreg__(104)
           LL += ml.y * f[q];
         }
         if (row_ok && X == 0 && hf == 0 && !(LL > 0.f) && p.err) atomicOr(p.err, 1);
+        if (!row_ok) continue;
+#pragma unroll 1
+        for (int c = 0; c < DQ / 16; ++c) {
+          float ov[16];
 #pragma unroll
-        for (int e = 0; e < DQ; ++e) ov[e] = 0.f;
-        for (int q = 0; q < wi.nparts; ++q) {
-          if (f[q] == 0.f) continue;
-          const float* src = p.part_o + ((base_unit + q) * 128 + row) * D + cw;
+          for (int e = 0; e < 16; ++e) ov[e] = 0.f;
+          for (int q = 0; q < wi.nparts; ++q) {
+            if (f[q] == 0.f) continue;
+            const float* src = p.part_o + ((base_unit + q) * 128 + row) * D + cw + c * 16;
 #pragma unroll
-          for (int e = 0; e < DQ; e += 4) {
-            const float4 x = __ldcg(reinterpret_cast<const float4*>(src + e));
-            ov[e] += x.x * f[q]; ov[e + 1] += x.y * f[q]; ov[e + 2] += x.z * f[q]; ov[e + 3] += x.w * f[q];
+            for (int e = 0; e < 16; e += 4) {
+              const float4 x = __ldcg(reinterpret_cast<const float4*>(src + e));
+              ov[e] += x.x * f[q]; ov[e + 1] += x.y * f[q]; ov[e + 2] += x.z * f[q]; ov[e + 3] += x.w * f[q];
+            }
           }
+          store_row<D, 16>(p, wi.h, grow, cw + c * 16, ov, 1.0f / LL);
         }
-        if (row_ok) {
-          store_row<D, DQ>(p, wi.h, grow, cw, ov, 1.0f / LL);
-          if (X == 0 && hf == 0 && p.lse)
-            p.lse[(long long)wi.h * p.Lq + grow] = (MM == -INFINITY ? -INFINITY : MM * p.scale) + logf(LL);
-        }
-        continue;
-      }
-      // ---- epilogue: O / L -> global
-      if (row_ok && X == 0 && hf == 0 && !(L > 0.f) && p.err) atomicOr(p.err, 1);
-      if (row_ok) {
-        store_row<D, DQ>(p, wi.h, grow, cw, ov, 1.0f / L);
         if (X == 0 && hf == 0 && p.lse)
-          p.lse[(long long)wi.h * p.Lq + grow] = (M == -INFINITY ? -INFINITY : M * p.scale) + logf(L);
+          p.lse[(long long)wi.h * p.Lq + grow] = (MM == -INFINITY ? -INFINITY : MM * p.scale) + logf(LL);
       }
     }
   }
