@@ -221,6 +221,11 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         const int b = it & 1;
         mbar_wait(s_full + b, (it >> 1) & 1);
         tc_fence_after();
+        if (p.debug == 1) {  // probe: tensor-core / TMA pipeline without softmax work
+          tc_fence_before();
+          mbar_arrive(p_full + b);
+          continue;
+        }
         const uint32_t s_col = C::COL_S + b * 128 + hf * KW;
         float v[KW];
 #pragma unroll

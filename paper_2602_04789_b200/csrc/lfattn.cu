@@ -537,6 +537,7 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
     }
     p.full_items = items - rem;
     p.tail_split = tail_split;
+    p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
     const int work = p.full_items + rem * tail_split;
     const int grid2 = work < slots ? work : slots;
     if (ver == 2) {
