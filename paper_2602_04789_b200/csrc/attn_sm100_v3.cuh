@@ -30,10 +30,11 @@ struct AttnCfg3 {
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int SEG_BYTES = 64 * 128;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;       // 2 stages
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;  // 2 stages
-  static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
-  static constexpr int SMEM = OFF_BAR + 256 + 2048 + 1024;  // barriers, row stats, align
+  static constexpr int KVST = 3;  // K and V ring stages (3 x 32 KB each at D = 128)
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KVST * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + KVST * KV_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024 + 1024;  // barriers, row stats (CG<=2), align
   static constexpr int TMEM_COLS = 512;
   static constexpr int COL_S = 0;    // + 128 * buffer
   static constexpr int COL_O = 256;
@@ -57,16 +58,17 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;    // [2]
-  uint64_t* k_empty = bars + 4;   // [2]
-  uint64_t* v_full = bars + 6;    // [2]
-  uint64_t* v_empty = bars + 8;   // [2]
-  uint64_t* s_full = bars + 10;   // [2]
-  uint64_t* p_full = bars + 12;   // [2]
-  uint64_t* pv_done = bars + 14;  // [2]
-  uint64_t* o_full = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
-  uint32_t* flag = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* k_full = bars + 2;    // [KVST]
+  uint64_t* k_empty = bars + 6;   // [KVST]
+  uint64_t* v_full = bars + 10;   // [KVST]
+  uint64_t* v_empty = bars + 14;  // [KVST]
+  uint64_t* s_full = bars + 18;   // [2]  S/P buffers
+  uint64_t* p_full = bars + 20;   // [2]
+  uint64_t* pv_done = bars + 22;  // [2]
+  uint64_t* o_full = bars + 24;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+  uint32_t* flag = reinterpret_cast<uint32_t*>(bars + 26);
+  static_assert(C::KVST <= 4, "barrier slots");
   float* red = reinterpret_cast<float*>(bars + 32);  // [CG][128] row maxima / sums
 
   const int warp = threadIdx.x >> 5;
@@ -75,11 +77,13 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::KVST; ++b) {
       mbar_init(k_full + b, 1);
       mbar_init(k_empty + b, 1);
       mbar_init(v_full + b, 1);
       mbar_init(v_empty + b, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(s_full + b, 1);
       mbar_init(p_full + b, 128 * CG);
       mbar_init(pv_done + b, 1);
@@ -110,8 +114,8 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
           tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, wi.tile * C::BM, wi.h);
         for (int j = cx.j0; j < cx.j1; ++j, ++it) {
           const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
-          const int st = it & 1;
-          const uint32_t par = ((it >> 1) & 1) ^ 1;
+          const int st = it % C::KVST;
+          const uint32_t par = ((it / C::KVST) & 1) ^ 1;
           mbar_wait(k_empty + st, par);
           mbar_expect_tx(k_full + st, C::KV_BYTES);
           for (int a = 0; a < C::ATOMS; ++a) {
@@ -137,18 +141,18 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
       constexpr uint32_t IDESC_PV = idesc_bf16(128, D, 0, 1);
       const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
       auto issue_pv = [&](uint32_t i2, bool first) {
-        const int b = i2 & 1;
-        const uint32_t par = (i2 >> 1) & 1;
-        mbar_wait(p_full + b, par);
-        mbar_wait(v_full + b, par);
+        const int b = i2 & 1;            // S/P buffer
+        const int st = i2 % C::KVST;     // V stage
+        mbar_wait(p_full + b, (i2 >> 1) & 1);
+        mbar_wait(v_full + st, (i2 / C::KVST) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < C::BN / 16; ++kk) {
-          uint64_t bd = smem_desc_sw128(v_base + b * C::KV_BYTES + kk * 16 * 128, C::BN * 128, 1024);
+          uint64_t bd = smem_desc_sw128(v_base + st * C::KV_BYTES + kk * 16 * 128, C::BN * 128, 1024);
           tc_mma_ts(tmem + C::COL_O, tmem + C::COL_S + b * 128 + kk * 8, bd, IDESC_PV,
                     (!first || kk > 0) ? 1u : 0u);
         }
-        tc_commit(v_empty + b);
+        tc_commit(v_empty + st);
         tc_commit(pv_done + b);
       };
       uint32_t it = 0, tc = 0;
@@ -157,8 +161,9 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         if (cx.j1 == cx.j0) continue;
         mbar_wait(q_full, tc++ & 1);
         for (int j = cx.j0; j < cx.j1; ++j, ++it) {
-          const int b = it & 1;
-          mbar_wait(k_full + b, (it >> 1) & 1);
+          const int b = it & 1;          // S/P buffer
+          const int st = it % C::KVST;   // K stage
+          mbar_wait(k_full + st, (it / C::KVST) & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
@@ -166,10 +171,10 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
             const uint32_t off = (kk & 3) * 32;
             uint64_t ad = smem_desc_sw128(q_base + a * (C::BM * 128) + off, 16, 1024);
             uint64_t bd =
-                smem_desc_sw128(k_base + b * C::KV_BYTES + a * (C::BN * 128) + off, 16, 1024);
+                smem_desc_sw128(k_base + st * C::KV_BYTES + a * (C::BN * 128) + off, 16, 1024);
             tc_mma_ss(tmem + C::COL_S + b * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
           }
-          tc_commit(k_empty + b);
+          tc_commit(k_empty + st);
           tc_commit(s_full + b);
           if (j == cx.j1 - 1) tc_commit(q_empty);
           if (j > cx.j0) issue_pv(it - 1, j - 1 == cx.j0);

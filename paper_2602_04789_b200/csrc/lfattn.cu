@@ -576,7 +576,7 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
                          AttnCfg3<DD>::SMEM);                                                   \
     attn_fwd_v3_kernel<DD, CGV><<<grid2, 64 + 128 * CGV, AttnCfg3<DD>::SMEM, S(stream)>>>(p, work); \
   }
-      LF_V3(128, 4) LF_V3(128, 2) LF_V3(64, 4) LF_V3(64, 2)
+      LF_V3(128, 2) LF_V3(64, 2)
 #undef LF_V3
     }
     return check_launch("attn_fwd_v2/v3_kernel");

@@ -73,6 +73,12 @@ class HsaRollout:
         return self.plan.s_device(i)
 
     # ------------------------------------------------------------------ API
+    def kv_slot(self, chunk_index: int):
+        """Device views (k, v) [H, f*n, d] of chunk i's cache slot, for producers
+        that write their K/V projections in place (then pass None to step)."""
+        sl = self._slot(int(chunk_index))
+        return self.kv_k[:, sl], self.kv_v[:, sl]
+
     def commit(self, k_clean: torch.Tensor, v_clean: torch.Tensor, chunk_index: int,
                overwrite: bool = False) -> None:
         """Append chunk i's clean K/V (rollout.py:306-308) and pool its summaries once.
@@ -88,8 +94,10 @@ class HsaRollout:
             raise ValueError(f"chunks must be committed in order: expected {self.committed + 1}, got {i}")
         lay.check_chunk(i)
         sl = self._slot(i)
-        self.kv_k[:, sl].copy_(k_clean)
-        self.kv_v[:, sl].copy_(v_clean)
+        if k_clean is not None:  # None: already written in place (kv_slot)
+            self.kv_k[:, sl].copy_(k_clean)
+        if v_clean is not None:
+            self.kv_v[:, sl].copy_(v_clean)
         # k_block rows of this chunk's frames
         spec = D.TilingSpec(lay.chunk_tokens, lay.n if self.framewise else lay.chunk_tokens,
                             lay.b_kv)
@@ -139,8 +147,10 @@ class HsaRollout:
         if self.committed != i - 1:
             raise ValueError(f"chunk {i} needs chunks 1..{i - 1} committed (have {self.committed})")
         sl = self._slot(i)
-        self.kv_k[:, sl].copy_(k_cur)
-        self.kv_v[:, sl].copy_(v_cur)
+        if k_cur is not None:  # None: the caller already wrote them in place (kv_slot)
+            self.kv_k[:, sl].copy_(k_cur)
+        if v_cur is not None:
+            self.kv_v[:, sl].copy_(v_cur)
         qt, kt = tilings(lay, i, self.framewise)
         P = (i - 1) * lay.f
         q_block = D.pool_blocks(q, qt)
