@@ -38,6 +38,7 @@ struct AttnCfg3 {
   static constexpr int TMEM_COLS = 512;
   static constexpr int COL_S = 0;    // + 128 * buffer
   static constexpr int COL_O = 256;
+  static constexpr int COL_Q = 384;  // Q as the TMEM A operand of QK^T (D/2 columns)
 };
 
 // CG = column groups per TMEM lane quarter: 4*CG softmax warps, each owning
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
   uint64_t* o_full = bars + 24;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
   uint32_t* flag = reinterpret_cast<uint32_t*>(bars + 26);
+  uint64_t* q_tmem = bars + 27;   // Q copied smem -> TMEM by the softmax warps
   static_assert(C::KVST <= 4, "barrier slots");
   float* red = reinterpret_cast<float*>(bars + 32);  // [CG][128] row maxima / sums
 
@@ -76,7 +78,8 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    mbar_init(q_empty, 128 * CG);
+    mbar_init(q_tmem, 128 * CG);
     for (int b = 0; b < C::KVST; ++b) {
       mbar_init(k_full + b, 1);
       mbar_init(k_empty + b, 1);
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
       for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
         const TileCtx cx = tile_ctx(p, work_item(p, w));
         if (cx.j1 == cx.j0) continue;
-        mbar_wait(q_full, tc++ & 1);
+        mbar_wait(q_tmem, tc++ & 1);
         for (int j = cx.j0; j < cx.j1; ++j, ++it) {
           const int b = it & 1;          // S/P buffer
           const int st = it % C::KVST;   // K stage
@@ -169,14 +172,14 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             const int a = kk >> 2;
             const uint32_t off = (kk & 3) * 32;
-            uint64_t ad = smem_desc_sw128(q_base + a * (C::BM * 128) + off, 16, 1024);
             uint64_t bd =
                 smem_desc_sw128(k_base + st * C::KV_BYTES + a * (C::BN * 128) + off, 16, 1024);
-            tc_mma_ss(tmem + C::COL_S + b * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
+            // A = Q from TMEM: only K is streamed from shared memory
+            tc_mma_ts(tmem + C::COL_S + b * 128, tmem + C::COL_Q + kk * 8, bd, IDESC_QK,
+                      kk > 0 ? 1u : 0u);
           }
           tc_commit(k_empty + st);
           tc_commit(s_full + b);
-          if (j == cx.j1 - 1) tc_commit(q_empty);
           if (j > cx.j0) issue_pv(it - 1, j - 1 == cx.j0);
         }
         issue_pv(it - 1, cx.j1 - 1 == cx.j0);
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
       }
       return r;
     };
-    uint32_t it = 0, tc = 0;
+    uint32_t it = 0, tc = 0, tq = 0;
     for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
@@ -220,6 +223,29 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         lq = lq < 32 ? lq : 31;
       }
       float m_used = -INFINITY, l = 0.f;
+      if (cx.j1 > cx.j0) {
+        // Q row (this warp's half of d) from the swizzled smem tile into TMEM
+        // columns COL_Q: bf16 pairs in K order, the A-operand layout of QK^T.
+        // The previous unit's QKs have all completed (its last s_full was seen).
+        mbar_wait(q_full, tq++ & 1);
+        constexpr int QW = D / CG / 8;  // 16-byte chunks of this warp's half row
+        const int e0 = hf * (D / CG);   // first column
+        uint32_t qr[QW * 4];
+#pragma unroll
+        for (int u = 0; u < QW; ++u) {
+          const int col = e0 + u * 8;
+          const int a = col >> 6, cu = (col & 63) >> 3;
+          const uint4 x = *reinterpret_cast<const uint4*>(
+              sQ + a * (C::BM * 128) + row * 128 + ((cu ^ (row & 7)) << 4));
+          qr[4 * u] = x.x; qr[4 * u + 1] = x.y; qr[4 * u + 2] = x.z; qr[4 * u + 3] = x.w;
+        }
+#pragma unroll
+        for (int c = 0; c < QW * 4; c += 16) tmem_st16(t_row + C::COL_Q + e0 / 2 + c, qr + c);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(q_tmem);
+        mbar_arrive(q_empty);
+      }
       for (int j = cx.j0; j < cx.j1; ++j, ++it) {
         const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
         const bool full = (ts.m0 & ts.m1) == -1 && ts.l0 == 64 && ts.l1 == 64;
