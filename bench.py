@@ -446,10 +446,21 @@ def run_ours(args, c):
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
+    except (OSError, ValueError):
         pass
-    tf_peak = peaks.get("bf16_tflops", 1590.0)
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tf_peak = peaks.get("bf16_tflops")
+    hbm_peak = peaks.get("hbm_gbs")
+    tf_src = "MEASURED_PEAKS.json bf16_tflops (burst), of measured"
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs, of measured"
+    if tf_peak is None:  # B200_PROFILING.md fallback when the driver file is absent
+        tf_peak, tf_src = 1590.0, "B200_PROFILING.md fallback 1.59 PFLOP/s burst, of fallback"
+    if hbm_peak is None:
+        hbm_peak, hbm_src = 6650.0, "B200_PROFILING.md fallback 6.65 TB/s, of fallback"
+    traffic = {}
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        pass
     flops_call = flops_local / T
     achieved_tf = flops_call / (attn_ms * 1e-3) / 1e12
     pool_bytes = h_local * (lq + lk) * d * 2 + h_local * (qt.count + kt.count + P) * d * 4
@@ -559,12 +570,16 @@ def run_ours(args, c):
                           "e2e_ms_per_chunk": e2e_ms_sl, "e2e_h2d_bytes_per_step": h2d_sl},
             "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel<128>",
                          "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
-                         "frac": achieved_tf / tf_peak, "traffic": None,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                         "frac": achieved_tf / tf_peak,
+                         "traffic": (traffic.get("attn_fwd", {}).get("bytes")
+                                     if args.config == "c2" else None),
+                         "traffic_source": traffic.get("attn_fwd", {}).get("source"),
+                         "peak_source": tf_src,
                          "attn_ms_per_call": attn_ms, "flops_per_call": flops_call},
             "roofline_select": {"bound": "hbm", "kernel": "pool_kernel (Q+K block pooling)",
                                 "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                                "frac": achieved_gbs / hbm_peak, "bytes_per_call": pool_bytes,
+                                "frac": achieved_gbs / hbm_peak, "peak_source": hbm_src,
+                                "bytes_per_call": pool_bytes,
                                 "pool_ms_per_call": pool_ms, "select_plan_ms_per_call": sel_ms},
             "cpu_baseline": cpu,
             "clocks": clk,

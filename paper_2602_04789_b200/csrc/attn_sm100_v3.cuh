@@ -43,7 +43,7 @@ struct AttnCfg3 {
 
 // CG = column groups per TMEM lane quarter: 4*CG softmax warps, each owning
 // 128/CG keys of S and D/CG columns of O for its 32 rows.
-template <int D, int CG>
+template <int D, int CG, int POLY = 0>
 __global__ void __launch_bounds__(64 + 128 * CG, 1)
     attn_fwd_v3_kernel(const __grid_constant__ AttnParams p, int total_work) {
   using C = AttnCfg3<D>;
@@ -299,8 +299,12 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
           for (int e = 0; e < 16; ++e) {
             float a, bb;
             f2unpack(ffma2(f2pack(v[32 * ch + 2 * e], v[32 * ch + 2 * e + 1]), c2v, nm), a, bb);
-            a = ex2(a);
-            bb = ex2(bb);
+            if (POLY > 0 && e % POLY == POLY - 1) {
+              exp2_poly2(a, bb);  // FMA-pipe exponentials for 1/POLY of the pairs
+            } else {
+              a = ex2(a);
+              bb = ex2(bb);
+            }
             acc[e & 3] = fadd2(acc[e & 3], f2pack(a, bb));
             pk[e] = pack_bf16(a, bb);
           }

@@ -488,7 +488,7 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (sms <= 0) sms = 148;
     }
-    static const int ver = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 4;
+    static const int ver = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 3;
     const int items = p.n_qtiles * q->heads;
     const int slots = (ver == 2 ? 2 : 1) * sms;  // v2: two co-resident CTAs per SM
     // split-KV balancing of the last, partial round: with items = k*slots + rem,
@@ -570,13 +570,15 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
       return LF_OK;
     } else {
       static const int cg = getenv("LF_ATTN_CG") ? atoi(getenv("LF_ATTN_CG")) : 2;
-#define LF_V3(DD, CGV)                                                                          \
-  if (q->d == DD && cg == CGV) {                                                                \
-    cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, CGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         AttnCfg3<DD>::SMEM);                                                   \
-    attn_fwd_v3_kernel<DD, CGV><<<grid2, 64 + 128 * CGV, AttnCfg3<DD>::SMEM, S(stream)>>>(p, work); \
+      static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
+#define LF_V3(DD, CGV, PV)                                                                      \
+  if (q->d == DD && cg == CGV && poly == PV) {                                                  \
+    cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, CGV, PV>,                                       \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg3<DD>::SMEM);      \
+    attn_fwd_v3_kernel<DD, CGV, PV><<<grid2, 64 + 128 * CGV, AttnCfg3<DD>::SMEM, S(stream)>>>(p, work); \
   }
-      LF_V3(128, 2) LF_V3(64, 2)
+      LF_V3(128, 2, 0) LF_V3(64, 2, 0) LF_V3(128, 2, 2) LF_V3(128, 2, 3) LF_V3(128, 2, 4)
+      LF_V3(128, 2, 8)
 #undef LF_V3
     }
     return check_launch("attn_fwd_v2/v3_kernel");

@@ -8,6 +8,6 @@ done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_c2.json 2> gpurun_out/bench_ref_c2.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --profile-launch --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 2 -c 1 -o gpurun_out/attn_c2 python bench.py --profile-launch --no-cpu-baseline > gpurun_out/ncu_attn.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:pool_kernel -s 2 -c 1 -o gpurun_out/pool_c2 python bench.py --profile-launch --no-cpu-baseline > gpurun_out/ncu_pool.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pool_frames -s 2 -c 1 -o gpurun_out/pool_c2 python bench.py --profile-launch --no-cpu-baseline > gpurun_out/ncu_pool.log 2>&1
 cat gpurun_out/bench_*.json
 tail -n 3 gpurun_out/*.err
