@@ -115,11 +115,17 @@ int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f,
                 double* alpha, double* s, int32_t* budgets, int32_t* clamped, double* scalars,
                 int32_t* status, void* stream);
 
-/* Per query tile (128 rows): union of its query blocks' active key blocks as
- * <=64-key segments {token start, length, query-block bitmask, 0}.  Segments
- * from block lists `blocks[H][nqb][cap]` / `count[H][nqb]` over the first
- * `list_blocks` key blocks of `k_tiling`.  Host-side replacement for the span
- * coalescing of attention.py:159-165,249-262. */
+/* Rows per tile plan (lf_plan_tile_rows(): 256 = a pair of 128-row query
+ * tiles, the unit of the attention kernel; 128 with LF_ATTN_VER=3). */
+int lf_plan_tile_rows(void);
+
+/* Per plan tile (lf_plan_tile_rows() rows): union of its query blocks' active
+ * key blocks as <=64-key segments {token start, length, query-block bitmask, 0}.
+ * Segments from block lists `blocks[H][nqb][cap]` / `count[H][nqb]` over the
+ * first `list_blocks` key blocks of `k_tiling`.  256-row plans are ordered in
+ * three classes (blocks used by both 128-row halves, by the first, by the
+ * second), each padded to an even count with {start, 0, 0, 0}.  Device-side
+ * replacement for the span coalescing of attention.py:159-165,249-262. */
 int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
                   int32_t cap, lf_tiling q_tiling, lf_tiling k_tiling, int32_t list_blocks,
                   int32_t seg_cap, int32_t* segs, int32_t* seg_count, void* stream);

@@ -26,7 +26,7 @@ LF_F32, LF_BF16 = 0, 1
 EXPORTS = (
     "lf_version", "lf_strerror", "lf_last_error", "lf_pool_blocks", "lf_compress", "lf_select",
     "lf_select_strided",
-    "lf_cag_plan", "lf_plan_tiles", "lf_attention", "lf_hsa_workspace_bytes", "lf_hsa_views",
+    "lf_cag_plan", "lf_plan_tile_rows", "lf_plan_tiles", "lf_attention", "lf_hsa_workspace_bytes", "lf_hsa_views",
     "lf_hsa_forward", "lf_rowdot", "lf_topk",
 )
 
@@ -67,6 +67,7 @@ _SIGS = {
                            _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "lf_cag_plan": ([ctypes.c_double, ctypes.c_double, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P,
                      _P, _P, _P, _P], ctypes.c_int),
+    "lf_plan_tile_rows": ([], ctypes.c_int),
     "lf_plan_tiles": ([_P, _P, _I, _I, _I, LfTiling, LfTiling, _I, _I, _P, _P, _P], ctypes.c_int),
     "lf_attention": ([ctypes.POINTER(LfMat), ctypes.POINTER(LfMat), ctypes.POINTER(LfMat), LfTiling,
                       _P, _P, _I, _I, _I, ctypes.c_float, _P, _I, ctypes.c_int64, ctypes.c_int64,

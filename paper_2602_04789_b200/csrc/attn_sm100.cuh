@@ -64,7 +64,8 @@ struct AttnParams {
   // tiles, the parts write unnormalised partials and the last one to finish
   // merges them (see attn_sm100_v2.cuh)
   int full_items, tail_split;
-  int debug;  // benchmarking probe: 1 = skip softmax arithmetic (P left as S bits)
+  int debug;  // benchmarking probe: 1 = skip softmax arithmetic (P left as S bits), 2 = trace
+  long long* trace;  // debug == 2: clock64 event trace of CTA 0 (v5)
   float* part_o;    // [tail*tail_split][128][D] fp32
   float2* part_ml;  // [tail*tail_split][128] (row max, row sum)
   int* counters;    // [tail], zero between launches

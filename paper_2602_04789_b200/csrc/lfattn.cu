@@ -10,6 +10,7 @@
 #include "attn_sm100_v2.cuh"
 #include "attn_sm100_v3.cuh"
 #include "attn_sm100_v4.cuh"
+#include "attn_sm100_v5.cuh"
 #include "cag.cuh"
 #include "pool.cuh"
 #include "select.cuh"
@@ -146,15 +147,164 @@ int launch_pool(PoolArgs& a, int dtype, int vec, int ns, cudaStream_t st) {
                           : launch_pool_t<float>(a, vec, ns, st);
 }
 
-int max_qblocks_per_tile(lf_tiling qt) {
+// attention kernel generation: 5 (default; query-tile pairs, 256-row plans)
+// or 3 (legacy single-tile kernel, 128-row plans), LF_ATTN_VER overrides
+int attn_ver() {
+  static const int v = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 3;
+  return v == 3 ? 3 : 5;
+}
+int plan_rows() { return attn_ver() == 5 ? 2 * kTileRows : kTileRows; }
+
+int max_qblocks_per_tile(lf_tiling qt, int rows = kTileRows) {
   Tiling t(qt);
   int worst = 0;
-  for (int q0 = 0; q0 < qt.total; q0 += kTileRows) {
-    int q1 = q0 + kTileRows < qt.total ? q0 + kTileRows : qt.total;
+  for (int q0 = 0; q0 < qt.total; q0 += rows) {
+    int q1 = q0 + rows < qt.total ? q0 + rows : qt.total;
     int n = t.block_of(q1 - 1) - t.block_of(q0) + 1;
     worst = n > worst ? n : worst;
   }
   return worst;
+}
+
+// segment capacity of one tile plan: <= mq query blocks x cap selected blocks,
+// <= all past blocks, each cut in ceil(b_kv/64) pieces, + 3 class pads
+int seg_cap_for(int mq, int cap_blocks, int list_blocks, int b_kv) {
+  const int pieces = (b_kv + kSegKeys - 1) / kSegKeys;
+  long long sc = (long long)mq * cap_blocks * pieces;
+  const long long all = (long long)list_blocks * pieces;
+  sc = sc < all ? sc : all;
+  sc += plan_rows() == kTileRows ? 0 : 3;
+  return sc > 0 ? (int)sc : 1;
+}
+
+// Split-KV scratch (partials + merge counters), grown outside graph capture and
+// never freed: captured CUDA graphs may still point at an older buffer.
+// Layout [counters][part_ml][part_o]; counters stay zero between launches.
+bool split_scratch(size_t need_c, size_t need_ml, size_t need_o, cudaStream_t st, int** counters,
+                   float2** part_ml, float** part_o) {
+  static void* ws = nullptr;
+  static size_t cap_c = 0, cap_ml = 0, cap_o = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (need_c > cap_c || need_ml > cap_ml || need_o > cap_o) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return false;
+    const size_t nc = need_c > cap_c ? need_c : cap_c, nm = need_ml > cap_ml ? need_ml : cap_ml,
+                 no = need_o > cap_o ? need_o : cap_o;
+    void* fresh = nullptr;
+    if (cudaMalloc(&fresh, nc + nm + no) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaMemsetAsync(fresh, 0, nc, st);
+    ws = fresh;
+    cap_c = nc;
+    cap_ml = nm;
+    cap_o = no;
+  }
+  char* b = static_cast<char*>(ws);
+  *counters = reinterpret_cast<int*>(b);
+  *part_ml = reinterpret_cast<float2*>(b + cap_c);
+  *part_o = reinterpret_cast<float*>(b + cap_c + cap_ml);
+  return true;
+}
+
+// v5: query-tile pairs; whole items round-robin, the tail (< grid items) stream-K
+int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
+  const int n_pairs = (p.n_qtiles + 1) / 2;
+  const int items = n_pairs * heads;
+  const int G = sms < AttnCfg5<128>::MAX_TAIL ? sms : AttnCfg5<128>::MAX_TAIL;
+  p.full_items = items / G * G;
+  const int R = items - p.full_items;
+  p.tail_split = 1;
+  p.part_o = nullptr;
+  p.part_ml = nullptr;
+  p.counters = nullptr;
+  if (R > 0) {
+    const size_t need_c = align_up((size_t)G * 4, 256);
+    const size_t need_ml = align_up((size_t)2 * G * 256 * 8, 256);
+    const size_t need_o = (size_t)2 * G * 256 * d * 4;
+    if (!split_scratch(need_c, need_ml, need_o, S(stream), &p.counters, &p.part_ml, &p.part_o)) {
+      p.counters = nullptr;
+      p.part_ml = nullptr;
+      p.part_o = nullptr;  // kernel falls back to whole tail items
+    }
+  }
+  const int grid = items < G && !p.part_o ? items : G;
+  if (grid <= 0) return LF_OK;
+  p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
+  if (p.debug == 2 && getenv("LF_ATTN_TRACE_CTA")) p.debug |= atoi(getenv("LF_ATTN_TRACE_CTA")) << 8;
+  if ((p.debug & 255) == 2) {
+    static long long* tr = nullptr;
+    if (!tr) {
+      cudaMalloc(&tr, 2048 * 8);
+      cudaMemset(tr, 0, 2048 * 8);
+    }
+    p.trace = tr;
+    static int dumps = 0;
+    if (dumps++ == 3) {  // dump after a few launches (ordered with the stream)
+      cudaStreamSynchronize(S(stream));
+      static long long h[2048];
+      cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
+      FILE* f = fopen("gpurun_out/attn_trace.txt", "w");
+      if (f) {
+        for (int i = 0; i < 2048; ++i) fprintf(f, "%lld\n", h[i]);
+        fclose(f);
+      }
+    }
+  }
+  static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
+#define LF_V5(DD, PV)                                                                         \
+  if (d == DD && poly == PV) {                                                                \
+    cudaFuncSetAttribute(attn_fwd_v5_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         AttnCfg5<DD>::SMEM);                                                 \
+    attn_fwd_v5_kernel<DD, PV><<<grid, 384, AttnCfg5<DD>::SMEM, S(stream)>>>(p, items, n_pairs); \
+    return check_launch("attn_fwd_v5_kernel");                                               \
+  }
+  LF_V5(128, 0) LF_V5(64, 0) LF_V5(128, 4) LF_V5(128, 8) LF_V5(128, 3) LF_V5(128, 2)
+#undef LF_V5
+  return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v5: d=%d poly=%d not instantiated", d, poly);
+}
+
+// v3 (legacy): one query tile per CTA, split-KV of the last partial round
+int launch_v3(AttnParams& p, int heads, int d, int sms, void* stream) {
+  const int items = p.n_qtiles * heads;
+  const int slots = sms;
+  int rem = items >= slots ? items % slots : items;
+  int tail_split = rem ? slots / rem : 1;
+  tail_split = tail_split > 4 ? 4 : tail_split;
+  if (const char* e = getenv("LF_ATTN_SPLIT")) {  // test hook: split every item
+    tail_split = atoi(e);
+    tail_split = tail_split < 1 ? 1 : (tail_split > 4 ? 4 : tail_split);
+    rem = items;
+  }
+  if (tail_split < 2) { rem = 0; tail_split = 1; }
+  if (rem > 0) {
+    const size_t need_c = align_up((size_t)rem * 4, 256);
+    const size_t need_ml = align_up((size_t)rem * tail_split * 128 * 8, 256);
+    const size_t need_o = (size_t)rem * tail_split * 128 * d * 4;
+    if (!split_scratch(need_c, need_ml, need_o, S(stream), &p.counters, &p.part_ml, &p.part_o)) {
+      rem = 0;
+      tail_split = 1;
+    }
+  }
+  p.full_items = items - rem;
+  p.tail_split = tail_split;
+  p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
+  const int work = p.full_items + rem * tail_split;
+  const int grid = work < slots ? work : slots;
+  static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
+#define LF_V3(DD, PV)                                                                         \
+  if (d == DD && poly == PV) {                                                                \
+    cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, 2, PV>,                                       \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg3<DD>::SMEM);    \
+    attn_fwd_v3_kernel<DD, 2, PV><<<grid, 320, AttnCfg3<DD>::SMEM, S(stream)>>>(p, work);     \
+    return check_launch("attn_fwd_v3_kernel");                                               \
+  }
+  LF_V3(128, 0) LF_V3(64, 0)
+#undef LF_V3
+  return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v3: d=%d poly=%d not instantiated", d, poly);
 }
 
 struct HsaGeom {
@@ -184,15 +334,13 @@ int hsa_geom(const lf_hsa_args* a, HsaGeom* g) {
   int kf = a->topk_frames < g->P ? a->topk_frames : g->P;
   g->frame_cap = kf > 0 ? kf : 1;
   g->cap = kf * g->bpf > 0 ? kf * g->bpf : 1;
-  g->ntiles = (Lq + kTileRows - 1) / kTileRows;
+  const int rows = plan_rows();
+  g->ntiles = (Lq + rows - 1) / rows;
   g->list_blocks = g->P * g->bpf;
-  int mq = max_qblocks_per_tile(g->qt);
-  if (mq > 32) return fail(LF_ERR_UNSUPPORTED, "b_q too small: %d query blocks per 128-row tile", mq);
-  int pieces = (a->b_kv + kSegKeys - 1) / kSegKeys;
-  long long sc = (long long)mq * (kf * g->bpf) * pieces;
-  long long all = (long long)g->list_blocks * pieces;
-  sc = sc < all ? sc : all;
-  g->seg_cap = sc > 0 ? (int)sc : 1;
+  int mq = max_qblocks_per_tile(g->qt, rows);
+  if (mq > 32)
+    return fail(LF_ERR_UNSUPPORTED, "b_q too small: %d query blocks per %d-row tile", mq, rows);
+  g->seg_cap = seg_cap_for(mq, kf * g->bpf, g->list_blocks, a->b_kv);
   g->dense_lo = g->P * a->n;
   g->dense_hi = Lk;
   return LF_OK;
@@ -232,6 +380,8 @@ HsaWs carve(const HsaGeom& g, void* base) {
 extern "C" {
 
 int lf_version(void) { return 100; }
+
+int lf_plan_tile_rows(void) { return plan_rows(); }
 
 const char* lf_strerror(int status) {
   switch (status) {
@@ -414,20 +564,21 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
   if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
   if ((rc = check_tiling(k_tiling, "k_tiling"))) return rc;
   if (!seg_count || !segs) return fail(LF_ERR_INVALID, "lf_plan_tiles: null output");
-  const int ntiles = (q_tiling.total + kTileRows - 1) / kTileRows;
+  const int rows = plan_rows();
+  const int ntiles = (q_tiling.total + rows - 1) / rows;
   if (list_blocks <= 0) {
     cudaMemsetAsync(seg_count, 0, (size_t)heads * ntiles * 4, S(stream));
     return check_launch("memset seg_count");
   }
   if (!blocks || !count) return fail(LF_ERR_INVALID, "lf_plan_tiles: null input");
-  if (max_qblocks_per_tile(q_tiling) > 32)
-    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per 128-row tile");
+  if (max_qblocks_per_tile(q_tiling, rows) > 32)
+    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per %d-row tile", rows);
   const int spw = list_blocks * 4;
   int wpc = (200 * 1024) / spw;
   if (wpc < 1) return fail(LF_ERR_UNSUPPORTED, "too many key blocks (%d)", list_blocks);
   wpc = wpc > 4 ? 4 : wpc;
   PlanArgs a{blocks, count, heads, nqb, cap, Tiling(q_tiling), Tiling(k_tiling), list_blocks,
-             ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc};
+             ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc, rows};
   const int smem = wpc * spw;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(plan_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -456,8 +607,8 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
         reinterpret_cast<uintptr_t>(m->ptr) % 16)
       return fail(LF_ERR_INVALID, "TMA needs 16-byte aligned rows");
   if (dense_lo < 0 || dense_hi > k->rows) return fail(LF_ERR_INVALID, "dense range outside keys");
-  if (max_qblocks_per_tile(q_tiling) > 32)
-    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per 128-row tile");
+  if (max_qblocks_per_tile(q_tiling, plan_rows()) > 32)
+    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per %d-row tile", plan_rows());
   if (!out) return fail(LF_ERR_INVALID, "null out");
   AttnParams p;
   memset(&p, 0, sizeof(p));
@@ -479,121 +630,15 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
   p.out_head_stride = out_head_stride;
   p.lse = lse;
   p.err = err_flag;
-  static const bool use_v1 = getenv("LF_ATTN_V1") != nullptr;
-  if (!use_v1) {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (sms <= 0) sms = 148;
-    }
-    static const int ver = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 3;
-    const int items = p.n_qtiles * q->heads;
-    const int slots = (ver == 2 ? 2 : 1) * sms;  // v2: two co-resident CTAs per SM
-    // split-KV balancing of the last, partial round: with items = k*slots + rem,
-    // the rem tail items are cut into s = slots/rem (<= 4) parts so every CTA
-    // finishes at about the same time (444 items on 296 slots: 296 whole items
-    // + 148 items in 2 parts).  Small problems (items < slots) split all items.
-    int rem = items >= slots ? items % slots : items;
-    int tail_split = rem ? slots / rem : 1;
-    tail_split = tail_split > 4 ? 4 : tail_split;
-    if (const char* e = getenv("LF_ATTN_SPLIT")) {  // test hook: split every item
-      tail_split = atoi(e);
-      tail_split = tail_split < 1 ? 1 : (tail_split > 4 ? 4 : tail_split);
-      rem = items;
-    }
-    if (tail_split < 2) { rem = 0; tail_split = 1; }
-    if (rem > 0) {
-      // workspace layout: [counters][part_ml][part_o]; counters stay at offset 0
-      // (zeroed once, reset by every merge), so any reuse keeps them valid
-      static void* ws = nullptr;
-      static size_t cap_c = 0, cap_ml = 0, cap_o = 0;
-      const size_t need_c = align_up((size_t)rem * 4, 256);
-      const size_t need_ml = align_up((size_t)rem * tail_split * 128 * 8, 256);
-      const size_t need_o = (size_t)rem * tail_split * 128 * q->d * 4;
-      if (need_c > cap_c || need_ml > cap_ml || need_o > cap_o) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        cudaStreamIsCapturing(S(stream), &cs);
-        void* fresh = nullptr;
-        const size_t nc = need_c > cap_c ? need_c : cap_c, nm = need_ml > cap_ml ? need_ml : cap_ml,
-                     no = need_o > cap_o ? need_o : cap_o;
-        // (the old buffer is kept alive: captured CUDA graphs may still point at it)
-        if (cs == cudaStreamCaptureStatusNone && cudaMalloc(&fresh, nc + nm + no) == cudaSuccess) {
-          cudaMemsetAsync(fresh, 0, nc, S(stream));
-          ws = fresh;
-          cap_c = nc; cap_ml = nm; cap_o = no;
-        } else {
-          rem = 0;
-          tail_split = 1;
-        }
-      }
-      if (rem > 0) {
-        char* b = static_cast<char*>(ws);
-        p.counters = reinterpret_cast<int*>(b);
-        p.part_ml = reinterpret_cast<float2*>(b + cap_c);
-        p.part_o = reinterpret_cast<float*>(b + cap_c + cap_ml);
-      }
-    }
-    p.full_items = items - rem;
-    p.tail_split = tail_split;
-    p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
-    const int work = p.full_items + rem * tail_split;
-    const int grid2 = work < slots ? work : slots;
-    if (ver == 2) {
-      if (q->d == 128) {
-        cudaFuncSetAttribute(attn_fwd_v2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             AttnCfg2<128>::SMEM);
-        attn_fwd_v2_kernel<128><<<grid2, 320, AttnCfg2<128>::SMEM, S(stream)>>>(p, work);
-      } else {
-        cudaFuncSetAttribute(attn_fwd_v2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             AttnCfg2<64>::SMEM);
-        attn_fwd_v2_kernel<64><<<grid2, 320, AttnCfg2<64>::SMEM, S(stream)>>>(p, work);
-      }
-    } else if (ver == 4) {
-      const void* fn = q->d == 128 ? (const void*)attn_fwd_v4_kernel<128>
-                                   : (const void*)attn_fwd_v4_kernel<64>;
-      const int smem = q->d == 128 ? AttnCfg4<128>::SMEM : AttnCfg4<64>::SMEM;
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (q->d == 128)
-        attn_fwd_v4_kernel<128><<<grid2, 576, smem, S(stream)>>>(p, work);
-      else
-        attn_fwd_v4_kernel<64><<<grid2, 576, smem, S(stream)>>>(p, work);
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) {
-        cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, fn);
-        return fail(LF_ERR_CUDA, "attn_fwd_v4_kernel: %s (regs %d, max threads %d, dyn smem %d/%d)",
-                    cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, smem,
-                    fa.maxDynamicSharedSizeBytes);
-      }
-      return LF_OK;
-    } else {
-      static const int cg = getenv("LF_ATTN_CG") ? atoi(getenv("LF_ATTN_CG")) : 2;
-      static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
-#define LF_V3(DD, CGV, PV)                                                                      \
-  if (q->d == DD && cg == CGV && poly == PV) {                                                  \
-    cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, CGV, PV>,                                       \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg3<DD>::SMEM);      \
-    attn_fwd_v3_kernel<DD, CGV, PV><<<grid2, 64 + 128 * CGV, AttnCfg3<DD>::SMEM, S(stream)>>>(p, work); \
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
   }
-      LF_V3(128, 2, 0) LF_V3(64, 2, 0) LF_V3(128, 2, 2) LF_V3(128, 2, 3) LF_V3(128, 2, 4)
-      LF_V3(128, 2, 8)
-#undef LF_V3
-    }
-    return check_launch("attn_fwd_v2/v3_kernel");
-  }
-  dim3 grid(p.n_qtiles, q->heads);
-  if (q->d == 128) {
-    cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         AttnCfg<128>::SMEM);
-    attn_fwd_kernel<128><<<grid, 192, AttnCfg<128>::SMEM, S(stream)>>>(p);
-  } else {
-    cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         AttnCfg<64>::SMEM);
-    attn_fwd_kernel<64><<<grid, 192, AttnCfg<64>::SMEM, S(stream)>>>(p);
-  }
-  return check_launch("attn_fwd_kernel");
+  if (attn_ver() == 5) return launch_v5(p, q->heads, q->d, sms, stream);
+  return launch_v3(p, q->heads, q->d, sms, stream);
 }
 
 size_t lf_hsa_workspace_bytes(const lf_hsa_args* a) {

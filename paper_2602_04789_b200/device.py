@@ -16,7 +16,12 @@ import torch
 from . import _lib as L
 
 SEG_KEYS = 64
-TILE_ROWS = 128
+TILE_ROWS = 128  # query rows per tcgen05 tile (one TMEM lane each)
+
+
+def plan_rows() -> int:
+    """Rows per tile plan: 256 (a pair of 128-row query tiles) unless the legacy kernel is selected."""
+    return int(L.lib().lf_plan_tile_rows())
 
 
 def _dev():
@@ -53,10 +58,10 @@ class TilingSpec:
         e = np.minimum(np.minimum(s + self.block, t * self.period + self.period), self.total)
         return np.stack([s, e], axis=1)
 
-    def max_blocks_per_tile(self) -> int:
+    def max_blocks_per_tile(self, rows: int = TILE_ROWS) -> int:
         worst = 0
-        for q0 in range(0, self.total, TILE_ROWS):
-            q1 = min(q0 + TILE_ROWS, self.total)
+        for q0 in range(0, self.total, rows):
+            q1 = min(q0 + rows, self.total)
             worst = max(worst, self.block_of(q1 - 1) - self.block_of(q0) + 1)
         return worst
 
@@ -175,10 +180,12 @@ def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
                seg_cap: int | None = None) -> TilePlan:
     lib = L.lib()
     H, nqb, cap = blocks.shape
-    ntiles = -(-qt.total // TILE_ROWS)
+    rows = plan_rows()
+    ntiles = -(-qt.total // rows)
     pieces = -(-kt.block // SEG_KEYS)
     if seg_cap is None:
-        seg_cap = max(1, min(qt.max_blocks_per_tile() * cap * pieces, max(list_blocks, 0) * pieces))
+        seg_cap = max(1, min(qt.max_blocks_per_tile(rows) * cap * pieces, max(list_blocks, 0) * pieces)
+                      + (3 if rows > TILE_ROWS else 0))
     dev = blocks.device
     segs = torch.empty((H, ntiles, seg_cap, 4), dtype=torch.int32, device=dev)
     seg_count = torch.empty((H, ntiles), dtype=torch.int32, device=dev)
