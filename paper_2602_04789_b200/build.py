@@ -42,7 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     tmp = OUT + ".tmp"
-    cmd = [nvcc(), *FLAGS, "-o", tmp, SRC]
+    extra = os.environ.get("LF_NVCC_FLAGS", "").split()  # e.g. -DLF_V5_TRACE (event trace builds)
+    cmd = [nvcc(), *FLAGS, *extra, "-o", tmp, SRC]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

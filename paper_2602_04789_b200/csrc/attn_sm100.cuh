@@ -66,6 +66,8 @@ struct AttnParams {
   int full_items, tail_split;
   int debug;  // benchmarking probe: 1 = skip softmax arithmetic (P left as S bits), 2 = trace
   long long* trace;  // debug == 2: clock64 event trace of CTA 0 (v5)
+  CUtensorMap to;    // v5: bf16 output map (box 64 cols x 32 rows), valid when tma_out
+  int tma_out;
   float* part_o;    // [tail*tail_split][128][D] fp32
   float2* part_ml;  // [tail*tail_split][128] (row max, row sum)
   int* counters;    // [tail], zero between launches

@@ -48,7 +48,9 @@ struct AttnCfg5 {
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + VST * KV_BYTES;
   static constexpr int MAX_TAIL = 160;             // >= gridDim.x - 1
-  static constexpr int OFF_TAIL = OFF_BAR + 256;   // int tailP[MAX_TAIL+1], A[MAX_TAIL+1], mode
+  static constexpr int QD = 4;                     // unit queue depth (scheduler -> roles)
+  static constexpr int OFF_UQ = OFF_BAR + 320;     // Unit5[QD], 64 B each
+  static constexpr int OFF_TAIL = OFF_UQ + 64 * QD;  // int tailP[MAX_TAIL+1], A[MAX_TAIL+1], mode
   static constexpr int SMEM = OFF_TAIL + 4 * (2 * MAX_TAIL + 4) + 1024;
   static_assert(SMEM <= 232448, "shared memory");
   static constexpr int TMEM_COLS = 512;
@@ -59,13 +61,22 @@ struct AttnCfg5 {
 
 // one unit of work: key tiles [j0, j1) of item `item`
 struct Unit5 {
-  int item, h, pair, T, j0, j1, nparts, part, cfirst, clast, tail;
+  int item, h, pair, T, j0, j1, nparts, part, cfirst, clast, tail, nseg;
+  uint32_t qm[2];  // query-block bits of tiles A and B (0: tile absent)
 };
+static_assert(sizeof(Unit5) <= 64, "unit queue slot");
 
 __device__ __forceinline__ int pair_T(const AttnParams& p, int item) {
   const int nseg = p.seg_count ? p.seg_count[item] : 0;
   const int dense = p.dense_hi > p.dense_lo ? p.dense_hi - p.dense_lo : 0;
   return ((nseg + 1) >> 1) + (dense + 127) / 128;
+}
+
+// 32 lanes x 8 columns of 32-bit: thread i writes lane (base+i)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -104,6 +115,22 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ long long gtime() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -116,8 +143,27 @@ __device__ __forceinline__ long long clk64() {
 }
 // trace layout (debug == 2, CTA 0, first 48 tiles): [X][tile][3] softmax
 // (wait start, S ready, P arrived) at 0; MMA [tile][X][2] (P seen, issued) at 512
+#ifdef LF_V5_TRACE
 #define LF_TRACE(idx, val) \
   if ((p.debug & 255) == 2 && (int)blockIdx.x == (p.debug >> 8) && p.trace) p.trace[idx] = (val)
+#else
+#define LF_TRACE(idx, val) \
+  do {                     \
+  } while (0)
+#endif
+
+// bit mask (relative to the pair's first query block) of the query blocks of tile X
+__device__ __forceinline__ uint32_t qmask_of(const AttnParams& p, int q0, int X) {
+  const int x0 = q0 + X * 128;
+  if (x0 >= p.Lq) return 0u;
+  int x1 = x0 + 128;
+  x1 = x1 < p.Lq ? x1 : p.Lq;
+  const int b0 = p.qt.block_of(q0);
+  int lo = p.qt.block_of(x0) - b0, hi = p.qt.block_of(x1 - 1) - b0;
+  hi = hi < 31 ? hi : 31;
+  const uint32_t upto = hi >= 31 ? 0xffffffffu : ((2u << hi) - 1u);
+  return upto & ~((1u << lo) - 1u);
+}
 
 // time weight of one key tile of item `item`: 4 with two query tiles, 3 with
 // one (the last pair of a head may have one)
@@ -144,17 +190,22 @@ struct UnitIter5 {
     }
     return lo;
   }
+  // Tail parts come first: a split item's partial writes and merge then overlap
+  // with the CTA's later whole items instead of ending the kernel.
   __device__ bool next(Unit5& u) {
     if (phase == 0) {
-      if (i < p.full_items) {
-        const int T = pair_T(p, i);
-        fill(u, i, T, 0, T, 1, 0, c, c, -1);
-        i += G;
-        return true;
-      }
+      if (tail_next(u)) return true;
       phase = 1;
-      k = 0;
     }
+    if (i < p.full_items) {
+      const int T = pair_T(p, i);
+      fill(u, i, T, 0, T, 1, 0, c, c, -1);
+      i += G;
+      return true;
+    }
+    return false;
+  }
+  __device__ bool tail_next(Unit5& u) {
     if (mode == 1) {  // tail items whole: CTA c takes tail item c
       if (k == 0 && c < R) {
         k = 1;
@@ -207,21 +258,26 @@ struct UnitIter5 {
     u.cfirst = cf;
     u.clast = cl;
     u.tail = tail;
+    u.nseg = p.seg_count ? p.seg_count[item] : 0;
+    const int q0 = u.pair * 256;
+    u.qm[0] = qmask_of(p, q0, 0);
+    u.qm[1] = qmask_of(p, q0, 1);
   }
 };
 
-// bit mask (relative to the pair's first query block) of the query blocks of tile X
-__device__ __forceinline__ uint32_t qmask_of(const AttnParams& p, int q0, int X) {
-  const int x0 = q0 + X * 128;
-  if (x0 >= p.Lq) return 0u;
-  int x1 = x0 + 128;
-  x1 = x1 < p.Lq ? x1 : p.Lq;
-  const int b0 = p.qt.block_of(q0);
-  int lo = p.qt.block_of(x0) - b0, hi = p.qt.block_of(x1 - 1) - b0;
-  hi = hi < 31 ? hi : 31;
-  const uint32_t upto = hi >= 31 ? 0xffffffffu : ((2u << hi) - 1u);
-  return upto & ~((1u << lo) - 1u);
+// consumer side of the unit queue (every lane of the warp pops; lane 0 frees)
+__device__ __forceinline__ bool pop_unit(Unit5* uq, uint64_t* full, uint64_t* empty, uint32_t& qi,
+                                         Unit5& u) {
+  constexpr int QD = AttnCfg5<128>::QD;
+  const int slot = qi % QD;
+  mbar_wait(full + slot, (qi / QD) & 1);
+  u = uq[slot];
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(empty + slot);
+  ++qi;
+  return u.item >= 0;
 }
+
 
 template <int D, int POLY>
 __global__ void __launch_bounds__(384, 1)
@@ -245,6 +301,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_empty = bars + 26;  // [VST]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
   int* flag = reinterpret_cast<int*>(bars + 31);
+  uint64_t* uq_full = bars + 32;   // [QD]
+  uint64_t* uq_empty = bars + 36;  // [QD]
+  Unit5* uq = reinterpret_cast<Unit5*>(smem + C::OFF_UQ);
   int* tail = reinterpret_cast<int*>(smem + C::OFF_TAIL);
   int* tail_mode = tail + 2 * C::MAX_TAIL + 2;
   static_assert(C::KST <= 4 && C::VST <= 4, "barrier slots");
@@ -258,7 +317,7 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) {
     for (int x = 0; x < 2; ++x) {
       mbar_init(q_full + x, 1);
-      mbar_init(q_empty + x, 1);
+      mbar_init(q_empty + x, 5);  // MMA commit + the 4 softmax warps of tile x
       mbar_init(s_full + x, 1);
       mbar_init(p_full + 2 * x, 128);
       mbar_init(p_full + 2 * x + 1, 128);
@@ -273,6 +332,10 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(v_full + b, 1);
       mbar_init(v_empty + b, 1);
     }
+    for (int b = 0; b < C::QD; ++b) {
+      mbar_init(uq_full + b, 1);
+      mbar_init(uq_empty + b, 10);  // producer, MMA and 8 softmax warps
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -283,43 +346,55 @@ __global__ void __launch_bounds__(384, 1)
     // Whole items [0, full_items) go round-robin (CTA c: c, c+G, ...); the
     // tail's cost is then shared out so that every CTA ends with about the
     // same total: CTA c gets tail range [A[c], A[c+1]) sized by its slack
-    // under the mean load.
+    // under the mean load.  All item costs are fetched with 8 loads in flight
+    // per lane (one L2 round trip per 256 items).
     int* tP = tail;
     int* A = tail + C::MAX_TAIL + 1;
     const int G = gridDim.x;
+    for (int cc = lane; cc <= G; cc += 32) A[cc] = 0;
+    __syncwarp();
+    for (int i0 = 0; i0 < total_items; i0 += 256) {
+      int cst[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int it = i0 + e * 32 + lane;
+        cst[e] = it < total_items ? p.seg_count ? p.seg_count[it] : 0 : 0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int it = i0 + e * 32 + lane;
+        if (it >= total_items) continue;
+        const int dense = p.dense_hi > p.dense_lo ? p.dense_hi - p.dense_lo : 0;
+        const int c = (((cst[e] + 1) >> 1) + (dense + 127) / 128) * pair_w(p, it, n_pairs);
+        if (it < p.full_items)
+          atomicAdd(&A[it % G], c);
+        else
+          tP[it - p.full_items] = c;
+      }
+    }
+    __syncwarp();
     int carry = 0;
     for (int k0 = 0; k0 < R; k0 += 32) {
       const int k = k0 + lane;
-      int cost = 0;
-      if (k < R) {
-        const int it = p.full_items + k;
-        cost = pair_T(p, it) * pair_w(p, it, n_pairs);
-      }
+      const int cost = k < R ? tP[k] : 0;
       int incl = cost;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
       }
+      __syncwarp();
       if (k < R) tP[k] = carry + incl - cost;
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     const int Wt = carry;
     int md = R <= 0 ? 0 : (Wt >= 8 * G && p.part_o ? 2 : 1);
     if (md == 2) {
-      // whole-item load per CTA (A[] doubles as scratch), total, slack prefix
-      long long tot = Wt;
-      for (int cc = lane; cc < G; cc += 32) {
-        int L = 0;
-        for (int it = cc; it < p.full_items; it += G) L += pair_T(p, it) * pair_w(p, it, n_pairs);
-        A[cc] = L;
-        tot += L;
-      }
+      long long tot = 0;
+      for (int cc = lane; cc < G; cc += 32) tot += A[cc];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      // tot was summed over lanes: the Wt term was added 32 times
-      tot -= 31LL * Wt;
-      __syncwarp();
+      tot += Wt;
       const double target = (double)tot / G;
       long long scar = 0;
       for (int c0 = 0; c0 < G; c0 += 32) {
@@ -366,12 +441,11 @@ __global__ void __launch_bounds__(384, 1)
       tma_prefetch(&p.tv);
     }
     __syncwarp();
-    UnitIter5 U(p, tail, mode, R, n_pairs);
     Unit5 u;
-    uint32_t kit = 0, nq0 = 0, nq1 = 0;
-    while (U.next(u)) {
+    uint32_t kit = 0, nq0 = 0, nq1 = 0, qi = 0;
+    while (pop_unit(uq, uq_full, uq_empty, qi, u)) {
       const int wid = u.item;
-      const int nseg = p.seg_count ? p.seg_count[wid] : 0;
+      const int nseg = u.nseg;
       const int4* segs = p.segs ? p.segs + (size_t)wid * p.seg_cap : nullptr;
       const int Tp = (nseg + 1) >> 1;
       const bool hasB = 2 * u.pair + 1 < p.n_qtiles;
@@ -436,16 +510,14 @@ __global__ void __launch_bounds__(384, 1)
     const uint64_t qd0 = smem_desc_sw128(q_base, 16, 1024);
     const uint64_t kd0 = smem_desc_sw128(k_base, 16, 1024);
     const uint64_t vd0 = smem_desc_sw128(v_base, C::BN * 128, 1024);
-    UnitIter5 U(p, tail, mode, R, n_pairs);
     Unit5 u;
-    uint32_t kit = 0, nq[2] = {0, 0}, np[2] = {0, 0}, noe[2] = {0, 0};
-    while (U.next(u)) {
+    uint32_t kit = 0, nq[2] = {0, 0}, np[2] = {0, 0}, noe[2] = {0, 0}, qi = 0;
+    while (pop_unit(uq, uq_full, uq_empty, qi, u)) {
       const int wid = u.item;
-      const int nseg = p.seg_count ? p.seg_count[wid] : 0;
+      const int nseg = u.nseg;
       const int4* segs = p.segs ? p.segs + (size_t)wid * p.seg_cap : nullptr;
       const int Tp = (nseg + 1) >> 1;
-      const int q0 = u.pair * 256;
-      const uint32_t qm[2] = {qmask_of(p, q0, 0), qmask_of(p, q0, 1)};
+      const uint32_t qm[2] = {u.qm[0], u.qm[1]};
       const bool has[2] = {u.j1 > u.j0, u.j1 > u.j0 && 2 * u.pair + 1 < p.n_qtiles};
 #pragma unroll
       for (int x = 0; x < 2; ++x)
@@ -526,6 +598,26 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     __syncwarp();
+  } else if (warp == 2) {
+    // ------------------------------------------------------------- unit scheduler
+    // resolves this CTA's units (global metadata loads included) ahead of the
+    // roles that consume them
+    UnitIter5 U(p, tail, mode, R, n_pairs);
+    Unit5 u;
+    uint32_t qi = 0;
+    bool more = true;
+    while (more) {
+      more = U.next(u);
+      if (!more) u.item = -1;
+      const int slot = qi % C::QD;
+      mbar_wait(uq_empty + slot, ((qi / C::QD) & 1) ^ 1);
+      if (lane == 0) {
+        uq[slot] = u;
+        mbar_arrive(uq_full + slot);  // release: the slot's contents are visible
+      }
+      __syncwarp();
+      ++qi;
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- softmax + epilogue
     const int X = (warp - 4) >> 2;  // query tile of the pair
@@ -535,16 +627,15 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t s_col = C::COL_S + X * 128;
     const uint32_t o_col = C::COL_O + X * 128;
     const float c2 = p.scale_log2;
-    UnitIter5 U(p, tail, mode, R, n_pairs);
     Unit5 u;
-    uint32_t ns = 0, no = 0, nu = 0;
-    while (U.next(u)) {
+    uint32_t ns = 0, no = 0, nu = 0, qi = 0;
+    while (pop_unit(uq, uq_full, uq_empty, qi, u)) {
       const int wid = u.item;
-      const int nseg = p.seg_count ? p.seg_count[wid] : 0;
+      const int nseg = u.nseg;
       const int4* segs = p.segs ? p.segs + (size_t)wid * p.seg_cap : nullptr;
       const int Tp = (nseg + 1) >> 1;
       const int q0 = u.pair * 256;
-      const uint32_t qm = qmask_of(p, q0, X);
+      const uint32_t qm = u.qm[X];
       const int grow = q0 + X * 128 + row;
       const bool row_ok = grow < p.Lq;
       int lq = 0;
@@ -607,44 +698,44 @@ __global__ void __launch_bounds__(384, 1)
           // O_X holds PV up to the previous tile (completed before S_X(j) was
           // signalled); rescale it before this tile's PV is released
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            float o[32];
-            tmem_ld32(t_row + o_col + c * 32, o);
+          for (int c = 0; c < D / 16; ++c) {
+            float o[16];
+            tmem_ld16(t_row + o_col + c * 16, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= factor;
-            tmem_st32(t_row + o_col + c * 32, o);
+            for (int e = 0; e < 16; ++e) o[e] *= factor;
+            tmem_st16(t_row + o_col + c * 16, reinterpret_cast<uint32_t*>(o));
           }
         }
         if (tr) LF_TRACE(X * 512 + (ns - 1) * 8 + 3, clk64());
         const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
         const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
-        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        uint64_t acc[2] = {0ull, 0ull};
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t pk[16];
+        for (int ch = 0; ch < 8; ++ch) {  // 16 keys (8 packed P columns) at a time
+          uint32_t pk[8];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          for (int e = 0; e < 8; ++e) {
             float a, bb;
-            f2unpack(ffma2(f2pack(v[32 * ch + 2 * e], v[32 * ch + 2 * e + 1]), c2v, nm), a, bb);
-            if (POLY > 0 && e % POLY == POLY - 1) {
+            f2unpack(ffma2(f2pack(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]), c2v, nm), a, bb);
+            if (POLY > 0 && (8 * (ch & 1) + e) % POLY == POLY - 1) {
               exp2_poly2(a, bb);
             } else {
               a = ex2(a);
               bb = ex2(bb);
             }
-            acc[e & 3] = fadd2(acc[e & 3], f2pack(a, bb));
+            acc[e & 1] = fadd2(acc[e & 1], f2pack(a, bb));
             pk[e] = pack_bf16(a, bb);
           }
-          tmem_st16(t_row + s_col + 16 * ch, pk);
-          if (ch == 1 || ch == 3) {  // a key half of P is in TMEM: release its PV
+          tmem_st8(t_row + s_col + 8 * ch, pk);
+          if (ch == 3 || ch == 7) {  // a key half of P is in TMEM: release its PV
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(p_full + 2 * X + (ch >> 1));
-            if (tr) LF_TRACE(X * 512 + (ns - 1) * 8 + 4 + (ch >> 1), clk64());
+            mbar_arrive(p_full + 2 * X + (ch >> 2));
+            if (tr) LF_TRACE(X * 512 + (ns - 1) * 8 + 4 + (ch >> 2), clk64());
           }
         }
-        acc[0] = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        acc[0] = fadd2(acc[0], acc[1]);
         float a, bb;
         f2unpack(acc[0], a, bb);
         l += a + bb;
@@ -658,6 +749,38 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
       }
       if (tru) LF_TRACE(X * 512 + 400 + nu * 4 + 1, clk64());
+      // Q_X is reusable once this unit's QKs are done (o_full covers them): the
+      // bf16 output tile is staged there (SW128, the TMA layout) and written with
+      // TMA stores, then the buffer goes back to the producer (q_empty)
+      const bool hasX = u.j1 > u.j0 && qm != 0;
+      const bool use_tma = p.tma_out && hasX;
+      unsigned char* stg = sQ + X * C::Q_BYTES;
+      auto stage16 = [&](int col0, const float* v, float inv) {  // 16 values at col0
+#pragma unroll
+        for (int h8 = 0; h8 < 2; ++h8) {
+          const int col = col0 + 8 * h8;
+          const int a = col >> 6, ch = (col & 63) >> 3;
+          const float* w = v + 8 * h8;
+          *reinterpret_cast<uint4*>(stg + a * (C::BM * 128) + row * 128 + ((ch ^ (row & 7)) << 4)) =
+              make_uint4(pack_bf16(w[0] * inv, w[1] * inv), pack_bf16(w[2] * inv, w[3] * inv),
+                         pack_bf16(w[4] * inv, w[5] * inv), pack_bf16(w[6] * inv, w[7] * inv));
+        }
+      };
+      auto tma_store_rows = [&]() {  // this warp's 32 staged rows -> out
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          for (int a = 0; a < C::ATOMS; ++a)
+            tma_store_3d(&p.to, stg + a * (C::BM * 128) + quarter * 32 * 128, a * 64,
+                         q0 + X * 128 + quarter * 32, u.h);
+          bulk_commit();
+          bulk_wait_read();
+        }
+        __syncwarp();
+      };
+      auto release_q = [&]() {
+        if (hasX && lane == 0) mbar_arrive(q_empty + X);
+      };
       if (u.nparts == 1) {
         // ---- whole item: O / l -> out
         if (row_ok && k == 0 && p.err) atomicOr(p.err, 1);  // no key at all (callers prevent)
@@ -670,7 +793,11 @@ __global__ void __launch_bounds__(384, 1)
           tmem_ld_wait();
           tc_fence_before();
           mbar_arrive(o_empty + X);  // O_X is free for the next unit's first PV
-          if (row_ok) {
+          if (use_tma) {
+#pragma unroll
+            for (int c = 0; c < D / 16; ++c) stage16(c * 16, o + 16 * c, inv);
+            tma_store_rows();
+          } else if (row_ok) {
 #pragma unroll
             for (int c = 0; c < D / 16; ++c) store_row<D, 16>(p, u.h, grow, c * 16, o + 16 * c, inv);
           }
@@ -678,28 +805,34 @@ __global__ void __launch_bounds__(384, 1)
             p.lse[(long long)u.h * p.Lq + grow] =
                 (m_used == -INFINITY ? -INFINITY : m_used * p.scale) + logf(l);
         }
+        release_q();
         if (tru) LF_TRACE(X * 512 + 400 + nu * 4 + 2, clk64());
         ++nu;
         continue;
       }
-      // ---- split item: publish this part's unnormalised O and (m, l); last part merges
+      // ---- split item: publish this part's unnormalised O and (m, l); the last
+      // part to finish merges all parts in CTA order (bit-reproducible).
+      // Partial layout [slot][X][D/4][128 rows] of float4: a warp's access to one
+      // column quad covers 32 consecutive rows (512 contiguous bytes).
       const int slot = blockIdx.x * 2 + (u.cfirst == (int)blockIdx.x ? 1 : 0);
-      const long long prow = (long long)slot * 256 + X * 128 + row;
+      auto part4 = [&](int sl) {
+        return reinterpret_cast<float4*>(p.part_o) + (long long)(sl * 2 + X) * (D / 4) * 128 + row;
+      };
       if (k > 0) {
+        float4* po = part4(slot);
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           float o[32];
           tmem_ld32(t_row + o_col + c * 32, o);
           tmem_ld_wait();
-          float* po = p.part_o + prow * D + c * 32;
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(po + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          for (int e = 0; e < 8; ++e)
+            po[(c * 8 + e) * 128] = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
         }
         tc_fence_before();
         mbar_arrive(o_empty + X);
       }
-      p.part_ml[prow] = make_float2(m_used, k > 0 ? l : 0.f);
+      p.part_ml[(long long)slot * 256 + X * 128 + row] = make_float2(m_used, k > 0 ? l : 0.f);
       if (tru) LF_TRACE(X * 512 + 460 + nu * 4, clk64());
       __threadfence();
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -714,49 +847,72 @@ __global__ void __launch_bounds__(384, 1)
       if (tru) LF_TRACE(X * 512 + 460 + nu * 4 + 1, clk64());
       if (tru) LF_TRACE(X * 512 + 460 + nu * 4 + 3, last ? 1 : 2);
       ++nu;
-      if (!last || !row_ok) continue;
+      if (!last) {
+        release_q();
+        continue;
+      }
       __threadfence();
-      // parts: the CTAs of [cfirst, clast] with non-empty tail ranges
+      const bool trm = tru && nu == 1;
+      if (trm) LF_TRACE(X * 512 + 480, clk64());
+      // parts: the CTAs of [cfirst, clast] with non-empty tail ranges, in order
       const int* A = tail + C::MAX_TAIL + 1;
-      auto slot_of = [&](int cc) { return cc * 2 + (cc == u.cfirst ? 1 : 0); };
       float M = -INFINITY;
       for (int cc = u.cfirst; cc <= u.clast; ++cc) {
         if (A[cc + 1] <= A[cc]) continue;
-        M = fmaxf(M, __ldcg(&p.part_ml[(long long)slot_of(cc) * 256 + X * 128 + row]).x);
+        const float2 ml = __ldcg(&p.part_ml[(long long)(cc * 2 + (cc == u.cfirst)) * 256 + X * 128 + row]);
+        if (ml.y > 0.f) M = fmaxf(M, ml.x);
       }
       float L = 0.f;
       for (int cc = u.cfirst; cc <= u.clast; ++cc) {
         if (A[cc + 1] <= A[cc]) continue;
-        const float2 ml = __ldcg(&p.part_ml[(long long)slot_of(cc) * 256 + X * 128 + row]);
-        L += (ml.y > 0.f && ml.x != -INFINITY) ? ml.y * ex2((ml.x - M) * c2) : 0.f;
+        const float2 ml = __ldcg(&p.part_ml[(long long)(cc * 2 + (cc == u.cfirst)) * 256 + X * 128 + row]);
+        if (ml.y > 0.f && ml.x != -INFINITY) L += ml.y * ex2((ml.x - M) * c2);
       }
-      if (!(L > 0.f) && p.err) atomicOr(p.err, 1);
+      if (row_ok && !(L > 0.f) && p.err) atomicOr(p.err, 1);
       const float inv = 1.0f / L;
+      if (trm) LF_TRACE(X * 512 + 481, clk64());
+      // 32-column quarters; a part with l = 0 never wrote its O, so its stale
+      // values must not reach the sum (not even as 0 * inf)
+      constexpr int QC = 32;
 #pragma unroll 1
-      for (int c = 0; c < D; c += 16) {
-        float ov[16];
+      for (int hf = 0; hf < D / QC; ++hf) {
+        float acc[QC];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) ov[e] = 0.f;
+        for (int e = 0; e < QC; ++e) acc[e] = 0.f;
         for (int cc = u.cfirst; cc <= u.clast; ++cc) {
           if (A[cc + 1] <= A[cc]) continue;
-          const long long r = (long long)slot_of(cc) * 256 + X * 128 + row;
-          const float2 ml = __ldcg(&p.part_ml[r]);
-          if (!(ml.y > 0.f) || ml.x == -INFINITY) continue;
-          const float f = ex2((ml.x - M) * c2);
-          const float* src = p.part_o + r * D + c;
+          const int sl = cc * 2 + (cc == u.cfirst);
+          const float2 ml = __ldcg(&p.part_ml[(long long)sl * 256 + X * 128 + row]);
+          const float4* src = part4(sl) + hf * (QC / 4) * 128;
+          float4 x4[QC / 4];
 #pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            const float4 x4 = __ldcg(reinterpret_cast<const float4*>(src + e));
-            ov[e] += x4.x * f; ov[e + 1] += x4.y * f; ov[e + 2] += x4.z * f; ov[e + 3] += x4.w * f;
+          for (int e = 0; e < QC / 4; ++e) x4[e] = __ldcg(src + e * 128);
+          const float f = (ml.y > 0.f && ml.x != -INFINITY) ? ex2((ml.x - M) * c2) : 0.f;
+          if (f != 0.f) {
+#pragma unroll
+            for (int e = 0; e < QC / 4; ++e) {
+              acc[4 * e] += x4[e].x * f; acc[4 * e + 1] += x4[e].y * f;
+              acc[4 * e + 2] += x4[e].z * f; acc[4 * e + 3] += x4[e].w * f;
+            }
           }
         }
-        store_row<D, 16>(p, u.h, grow, c, ov, inv);
+#pragma unroll
+        for (int c = 0; c < QC / 16; ++c) {
+          if (use_tma)
+            stage16(hf * QC + 16 * c, acc + 16 * c, inv);
+          else if (row_ok)
+            store_row<D, 16>(p, u.h, grow, hf * QC + 16 * c, acc + 16 * c, inv);
+        }
       }
-      if (p.lse)
+      if (use_tma) tma_store_rows();
+      if (trm) LF_TRACE(X * 512 + 490, clk64());
+      release_q();
+      if (row_ok && p.lse)
         p.lse[(long long)u.h * p.Lq + grow] = (M == -INFINITY ? -INFINITY : M * p.scale) + logf(L);
       if (tru) LF_TRACE(X * 512 + 460 + (nu - 1) * 4 + 2, clk64());
     }
   }
+  if (warp >= 4 && lane == 0) bulk_wait_all();  // TMA output stores complete
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

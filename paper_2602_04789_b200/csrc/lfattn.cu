@@ -60,6 +60,19 @@ EncodeTiledFn encoder() {
 }
 
 // 3-D map (d, rows, heads) over a bf16 lf_mat, 64-column x box_rows boxes, 128B swizzle
+// bf16 output [H][Lq][d] (row / head strides in elements) for the v5 TMA-store epilogue
+bool make_out_map(CUtensorMap* map, void* out, int d, int Lq, int H, long long rs, long long hs) {
+  EncodeTiledFn enc = encoder();
+  if (!enc || reinterpret_cast<uintptr_t>(out) % 16 || (rs * 2) % 16 || (hs * 2) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)Lq, (cuuint64_t)H};
+  cuuint64_t strides[2] = {(cuuint64_t)rs * 2, (cuuint64_t)hs * 2};
+  cuuint32_t box[3] = {64, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, out, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int make_map(CUtensorMap* map, const lf_mat* m, int box_rows) {
   EncodeTiledFn enc = encoder();
   if (!enc) return fail(LF_ERR_NO_DRIVER, "cuTensorMapEncodeTiled unavailable");
@@ -637,7 +650,11 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  if (attn_ver() == 5) return launch_v5(p, q->heads, q->d, sms, stream);
+  if (attn_ver() == 5) {
+    p.tma_out = out_dtype == LF_BF16 && !getenv("LF_ATTN_NO_TMA_OUT") &&
+                make_out_map(&p.to, out, q->d, q->rows, q->heads, out_row_stride, out_head_stride);
+    return launch_v5(p, q->heads, q->d, sms, stream);
+  }
   return launch_v3(p, q->heads, q->d, sms, stream);
 }
 

@@ -2,7 +2,7 @@
 #   SWEEP="LF_ATTN_POLY=0 LF_ATTN_POLY=4" CONFIGS="c2 c5_dense" bash scripts/gpu_sweep.sh
 python -c "import __graft_entry__ as g; g.build()" > /dev/null
 if [ -n "$TESTS" ]; then
-  timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$? >> gpurun_out/pytest_gpu.log
+  env $TESTENV timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$? >> gpurun_out/pytest_gpu.log
   tail -n 2 gpurun_out/pytest_gpu.log
 fi
 for sw in ${SWEEP:-NONE=0}; do

@@ -31,3 +31,7 @@ for X in range(2):
         v = [t[X * 512 + 460 + u * 4 + i] for i in range(4)]
         if any(v):
             print("unit", u, "X", X, "split (partial written, counter done, merge done, last?):", [r(x) for x in v[:3]], v[3])
+for X in range(2):
+    v = [t[X * 512 + 480 + i] for i in range(11)]
+    if v[0]:
+        print("merge X", X, "deltas:", [v[i] - v[0] if v[i] else None for i in range(11)])
