@@ -268,7 +268,7 @@ def run_ours(args, c):
     V = [gen(s + 200, lk, h0) for s in range(T)]
     pipes = [lf.HsaPipeline(lay, h_local, i, cfg, framewise=True, out_dtype=torch.bfloat16)
              for _ in range(T)]
-    outs = [p.bind(Q[s], K[s], V[s], s_dev) for s, p in enumerate(pipes)]
+    outs = [p.bind(Q[s], K[s], V[s], s_dev, s_host=s_host) for s, p in enumerate(pipes)]
     full = [torch.empty((H, lq, d), dtype=torch.bfloat16, device=dev) for _ in range(T)] \
         if mode == "headshard" else None
 
@@ -351,13 +351,13 @@ def run_ours(args, c):
         if i > 1:
             ro.commit(None, None, i - 1, overwrite=True)
         for s in range(T):
-            ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s])
+            ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s], s_host=s_host)
             if mode == "headshard":
                 gather_heads(r_out[s], shard, out=full[s])
 
     flops_r = 0
     for s in range(T):
-        ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s])
+        ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s], s_host=s_host)
         flops_r += ro.selection_flops()
     for _ in range(max(args.warmup, 3)):
         chunk_flow()
@@ -394,6 +394,9 @@ def run_ours(args, c):
     qt, kt = tilings(lay, i, True)
     bpf = lay.frame_kv_blocks
     P = (i - 1) * f
+    hint = D.past_tiles_hint(s_host, i, f, bpf, c["topk"], qt)
+    from paper_2602_04789_b200 import _lib as LL
+    kernel_used = int(LL.lib().lf_attention_kernel_choice(h_local, lq, lq, hint))
     stage = {"pool": [], "select": [], "attn": []}
     graphs = []
     for s in range(T):
@@ -408,7 +411,8 @@ def run_ours(args, c):
             st["tiles"] = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf)
 
         def run_attn(s=s, st=st):
-            D.attention(Q[s], K[s], V[s], qt, st["tiles"], P * n, lk, out=outs[s])
+            D.attention(Q[s], K[s], V[s], qt, st["tiles"], P * n, lk, out=outs[s],
+                        past_tiles=hint)
 
         fns = (run_pool, run_sel, run_attn)
         for fn in fns:  # warm (allocates the static buffers the graphs reuse)
@@ -525,7 +529,7 @@ def run_ours(args, c):
             kc, vc = ro.kv_slot(i)
             kc.copy_(hkc[s], non_blocking=True)
             vc.copy_(hvc[s], non_blocking=True)
-            ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s])
+            ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s], s_host=s_host)
             if mode == "headshard":
                 gather_heads(r_out[s], shard, out=full[s])
             hro[s].copy_(r_out[s], non_blocking=True)
@@ -568,7 +572,9 @@ def run_ours(args, c):
                           "api": "HsaPipeline / lf_hsa_forward, full K/V per call",
                           "e2e_value": flops_step / (e2e_ms_sl * 1e-3) / 1e12,
                           "e2e_ms_per_chunk": e2e_ms_sl, "e2e_h2d_bytes_per_step": h2d_sl},
-            "roofline": {"bound": "tensor", "kernel": "attn_fwd_kernel<128>",
+            "roofline": {"bound": "tensor",
+                         "kernel": ("attn_fwd_v5_kernel<128> (query-tile pairs)" if kernel_used == 5
+                                    else "attn_fwd_v3_kernel<128> (one query tile per CTA)"),
                          "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
                          "frac": achieved_tf / tf_peak,
                          "traffic": (traffic.get("attn_fwd", {}).get("bytes")

@@ -116,7 +116,7 @@ int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f,
                 int32_t* status, void* stream);
 
 /* Rows per tile plan (lf_plan_tile_rows(): 256 = a pair of 128-row query
- * tiles, the unit of the attention kernel; 128 with LF_ATTN_VER=3). */
+ * tiles; both attention kernels read these plans). */
 int lf_plan_tile_rows(void);
 
 /* Per plan tile (lf_plan_tile_rows() rows): union of its query blocks' active
@@ -144,6 +144,26 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
                  int64_t out_row_stride, int64_t out_head_stride, float* lse, int32_t* err_flag,
                  void* stream);
 
+/* lf_attention with an explicit kernel choice (same results within the stated
+ * tolerance, bit-exact masks either way):
+ *   LF_KERNEL_AUTO  work-based choice from past_tiles_hint (estimated non-dense
+ *                   key tiles per 256-row plan tile; -1 = unknown -> 0)
+ *   LF_KERNEL_TILE  one 128-row query tile per CTA (best for short work per SM)
+ *   LF_KERNEL_PAIR  two query tiles per CTA in ping-pong sharing K/V, stream-K
+ *                   tail (best for long work per SM) */
+#define LF_KERNEL_AUTO 0
+#define LF_KERNEL_TILE 3
+#define LF_KERNEL_PAIR 5
+/* The kernel LF_KERNEL_AUTO picks for this problem (reporting). */
+int lf_attention_kernel_choice(int32_t heads, int32_t q_rows, int32_t dense_keys,
+                               int32_t past_tiles_hint);
+int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                    const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                    int32_t dense_lo, int32_t dense_hi, float scale, void* out,
+                    int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
+                    float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
+                    void* stream);
+
 /* One full hot-path call for all heads of one layer at one denoising step of
  * chunk i: compress -> select -> plan tiles -> sparse attention.  Replaces
  * selection.py:196-231 (hsa_attention).  Workspace from lf_hsa_workspace_bytes. */
@@ -160,6 +180,8 @@ typedef struct {
   int64_t out_row_stride, out_head_stride;
   float* lse;               /* optional                                       */
   int32_t* err_flag;        /* optional                                       */
+  int32_t attn_kernel;      /* LF_KERNEL_AUTO / _TILE / _PAIR                 */
+  double s_i_host;          /* host copy of s_i for LF_KERNEL_AUTO (NaN: unknown) */
 } lf_hsa_args;
 
 size_t lf_hsa_workspace_bytes(const lf_hsa_args* a);

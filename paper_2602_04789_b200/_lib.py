@@ -21,12 +21,14 @@ LIB_PATH = os.path.join(_HERE, "_lib", "liblfattn.so")
 LF_OK, LF_ERR_INVALID, LF_ERR_CUDA, LF_ERR_UNSUPPORTED = 0, 1, 2, 3
 LF_ERR_ZERO_ACTIVE_ROW, LF_ERR_DEGENERATE, LF_ERR_NO_DRIVER = 4, 5, 6
 LF_F32, LF_BF16 = 0, 1
+LF_KERNEL_AUTO, LF_KERNEL_TILE, LF_KERNEL_PAIR = 0, 3, 5
 
 # every symbol include/lfattn.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "lf_version", "lf_strerror", "lf_last_error", "lf_pool_blocks", "lf_compress", "lf_select",
     "lf_select_strided",
-    "lf_cag_plan", "lf_plan_tile_rows", "lf_plan_tiles", "lf_attention", "lf_hsa_workspace_bytes", "lf_hsa_views",
+    "lf_cag_plan", "lf_plan_tile_rows", "lf_plan_tiles", "lf_attention", "lf_attention_ex",
+    "lf_attention_kernel_choice", "lf_hsa_workspace_bytes", "lf_hsa_views",
     "lf_hsa_forward", "lf_rowdot", "lf_topk",
 )
 
@@ -49,7 +51,8 @@ class LfHsaArgs(ctypes.Structure):
                 ("per_frame_mode", ctypes.c_int32), ("s_i_dev", ctypes.c_void_p),
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
                 ("out_row_stride", ctypes.c_int64), ("out_head_stride", ctypes.c_int64),
-                ("lse", ctypes.c_void_p), ("err_flag", ctypes.c_void_p)]
+                ("lse", ctypes.c_void_p), ("err_flag", ctypes.c_void_p),
+                ("attn_kernel", ctypes.c_int32), ("s_i_host", ctypes.c_double)]
 
 
 _P = ctypes.c_void_p
@@ -72,6 +75,10 @@ _SIGS = {
     "lf_attention": ([ctypes.POINTER(LfMat), ctypes.POINTER(LfMat), ctypes.POINTER(LfMat), LfTiling,
                       _P, _P, _I, _I, _I, ctypes.c_float, _P, _I, ctypes.c_int64, ctypes.c_int64,
                       _P, _P, _P], ctypes.c_int),
+    "lf_attention_ex": ([ctypes.POINTER(LfMat), ctypes.POINTER(LfMat), ctypes.POINTER(LfMat),
+                         LfTiling, _P, _P, _I, _I, _I, ctypes.c_float, _P, _I, ctypes.c_int64,
+                         ctypes.c_int64, _P, _P, _I, _I, _P], ctypes.c_int),
+    "lf_attention_kernel_choice": ([_I, _I, _I, _I], ctypes.c_int),
     "lf_hsa_workspace_bytes": ([ctypes.POINTER(LfHsaArgs)], ctypes.c_size_t),
     "lf_hsa_views": ([ctypes.POINTER(LfHsaArgs), _P] + [ctypes.POINTER(_P)] * 7 +
                      [ctypes.POINTER(_I), ctypes.POINTER(_I)], ctypes.c_int),

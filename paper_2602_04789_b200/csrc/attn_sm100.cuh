@@ -68,6 +68,7 @@ struct AttnParams {
   long long* trace;  // debug == 2: clock64 event trace of CTA 0 (v5)
   CUtensorMap to;    // v5: bf16 output map (box 64 cols x 32 rows), valid when tma_out
   int tma_out;
+  int plan_pairs;    // segs are 256-row (pair) plans
   float* part_o;    // [tail*tail_split][128][D] fp32
   float2* part_ml;  // [tail*tail_split][128] (row max, row sum)
   int* counters;    // [tail], zero between launches

@@ -86,13 +86,30 @@ __device__ __forceinline__ WorkItem work_item(const AttnParams& p, int u) {
 }
 
 struct TileCtx {
-  int nseg, Tp, T;  // T = all key tiles of the item
+  int nseg, Tp, T;  // T = all key tiles of the item's plan
   int j0, j1;       // this part's key tiles [j0, j1)
   const int4* segs;
+  uint32_t qm;      // query-block bits of this 128-row tile in its plan (all: 128-row plans)
+  int q0;           // first row of the plan tile (qmask bits are relative to its block)
 };
+__device__ __forceinline__ uint32_t tile_qmask(const AttnParams& p, int q0, int x0) {
+  if (x0 >= p.Lq) return 0u;
+  int x1 = x0 + 128;
+  x1 = x1 < p.Lq ? x1 : p.Lq;
+  const int b0 = p.qt.block_of(q0);
+  int lo = p.qt.block_of(x0) - b0, hi = p.qt.block_of(x1 - 1) - b0;
+  hi = hi < 31 ? hi : 31;
+  const uint32_t upto = hi >= 31 ? 0xffffffffu : ((2u << hi) - 1u);
+  return upto & ~((1u << lo) - 1u);
+}
+// v3 on pair plans (p.plan_pairs): a 128-row tile reads its pair's class-ordered
+// list and skips the key tiles only its partner needs
 __device__ __forceinline__ TileCtx tile_ctx(const AttnParams& p, WorkItem wi) {
   TileCtx c;
-  const int wid = wi.h * p.n_qtiles + wi.tile;
+  const int n_pairs = (p.n_qtiles + 1) >> 1;
+  const int wid = p.plan_pairs ? wi.h * n_pairs + (wi.tile >> 1) : wi.h * p.n_qtiles + wi.tile;
+  c.q0 = p.plan_pairs ? (wi.tile >> 1) * 256 : wi.tile * 128;
+  c.qm = p.plan_pairs ? tile_qmask(p, c.q0, wi.tile * 128) : 0xffffffffu;
   c.nseg = p.seg_count ? p.seg_count[wid] : 0;
   c.segs = p.segs ? p.segs + (size_t)wid * p.seg_cap : nullptr;
   c.Tp = (c.nseg + 1) >> 1;

@@ -115,10 +115,12 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         mbar_expect_tx(q_full, C::Q_BYTES);
         for (int a = 0; a < C::ATOMS; ++a)
           tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, wi.tile * C::BM, wi.h);
-        for (int j = cx.j0; j < cx.j1; ++j, ++it) {
+        for (int j = cx.j0; j < cx.j1; ++j) {
           const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
+          if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;  // partner tile's keys only
           const int st = it % C::KVST;
           const uint32_t par = ((it / C::KVST) & 1) ^ 1;
+          ++it;
           mbar_wait(k_empty + st, par);
           mbar_expect_tx(k_full + st, C::KV_BYTES);
           for (int a = 0; a < C::ATOMS; ++a) {
@@ -163,7 +165,10 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         const TileCtx cx = tile_ctx(p, work_item(p, w));
         if (cx.j1 == cx.j0) continue;
         mbar_wait(q_tmem, tc++ & 1);
-        for (int j = cx.j0; j < cx.j1; ++j, ++it) {
+        int done = 0;
+        for (int j = cx.j0; j < cx.j1; ++j) {
+          const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
+          if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;
           const int b = it & 1;          // S/P buffer
           const int st = it % C::KVST;   // K stage
           mbar_wait(k_full + st, (it / C::KVST) & 1);
@@ -180,10 +185,14 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
           }
           tc_commit(k_empty + st);
           tc_commit(s_full + b);
-          if (j > cx.j0) issue_pv(it - 1, j - 1 == cx.j0);
+          if (done > 0) issue_pv(it - 1, done == 1);
+          ++it;
+          ++done;
         }
-        issue_pv(it - 1, cx.j1 - 1 == cx.j0);
-        tc_commit(o_full);
+        if (done > 0) {
+          issue_pv(it - 1, done == 1);
+          tc_commit(o_full);
+        }
       }
     }
     __syncwarp();
@@ -219,9 +228,10 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
       const bool row_ok = grow < p.Lq;
       int lq = 0;
       if (row_ok) {
-        lq = p.qt.block_of(grow) - p.qt.block_of(q0);
+        lq = p.qt.block_of(grow) - p.qt.block_of(cx.q0);
         lq = lq < 32 ? lq : 31;
       }
+      int kdone = 0;
       float m_used = -INFINITY, l = 0.f;
       if (cx.j1 > cx.j0) {
         // Q row (this warp's half of d) from the swizzled smem tile into TMEM
@@ -246,8 +256,10 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         mbar_arrive(q_tmem);
         mbar_arrive(q_empty);
       }
-      for (int j = cx.j0; j < cx.j1; ++j, ++it) {
+      for (int j = cx.j0; j < cx.j1; ++j) {
         const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
+        if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;
+        ++kdone;
         const bool full = (ts.m0 & ts.m1) == -1 && ts.l0 == 64 && ts.l1 == 64;
         const int b = it & 1;
         mbar_wait(s_full + b, (it >> 1) & 1);
@@ -255,6 +267,7 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         if (p.debug == 1) {  // probe: tensor-core / TMA pipeline without softmax work
           tc_fence_before();
           mbar_arrive(p_full + b);
+          ++it;
           continue;
         }
         const uint32_t s_col = C::COL_S + b * 128 + hf * KW;
@@ -280,7 +293,7 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         const float m_new = fmaxf(m_used, mt);
         const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
         const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
-        const bool rescale = __any_sync(0xffffffffu, need) && j > cx.j0;
+        const bool rescale = __any_sync(0xffffffffu, need) && kdone > 1;
         if (need) {
           l *= factor;
           m_used = m_new;
@@ -333,12 +346,13 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
         tc_fence_before();
         mbar_arrive(p_full + b);
         pair_sync();  // red[] is reused by the next tile
+        ++it;
       }
       if (cx.T == 0) {
         if (row_ok && p.err) atomicOr(p.err, 1);  // no key at all (callers prevent this)
         continue;
       }
-      const bool empty_part = cx.j1 == cx.j0;
+      const bool empty_part = kdone == 0;
       l = group_other(l, false);
       pair_sync();
       if (!empty_part) {

@@ -79,6 +79,16 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
                : "memory");
 }
 
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ void unpack_f16(uint32_t v, float& a, float& b) {
+  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
+      : "=f"(a), "=f"(b) : "r"(v));
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -190,8 +200,9 @@ struct UnitIter5 {
     }
     return lo;
   }
-  // Tail parts come first: a split item's partial writes and merge then overlap
-  // with the CTA's later whole items instead of ending the kernel.
+  // Order: tail parts, then whole items (the scheduler pushes the CTA's first
+  // whole item before this), so a split item's partial writes and merge overlap
+  // with later whole items where there are any.
   __device__ bool next(Unit5& u) {
     if (phase == 0) {
       if (tail_next(u)) return true;
@@ -311,6 +322,9 @@ __global__ void __launch_bounds__(384, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int R = total_items - p.full_items;
+#ifdef LF_V5_TRACE
+  int st_units_g = 0, st_merges_g = 0, st_split_g = 0;
+#endif
   if ((p.debug & 255) == 2 && p.trace && threadIdx.x == 0) p.trace[1536 + 2 * blockIdx.x] = gtime();
   LF_TRACE(1840, clk64());
 
@@ -339,97 +353,10 @@ __global__ void __launch_bounds__(384, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
-  if (warp == 2) {
-    // ---- tail table.  cost(item) = key tiles x pair_w: 4 per tile for two
-    // query tiles, 3 for one (a lone query tile's softmax/MMA chain has no
-    // partner to overlap with, so it costs 3/4 of a pair's time, not 1/2).
-    // Whole items [0, full_items) go round-robin (CTA c: c, c+G, ...); the
-    // tail's cost is then shared out so that every CTA ends with about the
-    // same total: CTA c gets tail range [A[c], A[c+1]) sized by its slack
-    // under the mean load.  All item costs are fetched with 8 loads in flight
-    // per lane (one L2 round trip per 256 items).
-    int* tP = tail;
-    int* A = tail + C::MAX_TAIL + 1;
-    const int G = gridDim.x;
-    for (int cc = lane; cc <= G; cc += 32) A[cc] = 0;
-    __syncwarp();
-    for (int i0 = 0; i0 < total_items; i0 += 256) {
-      int cst[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int it = i0 + e * 32 + lane;
-        cst[e] = it < total_items ? p.seg_count ? p.seg_count[it] : 0 : 0;
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int it = i0 + e * 32 + lane;
-        if (it >= total_items) continue;
-        const int dense = p.dense_hi > p.dense_lo ? p.dense_hi - p.dense_lo : 0;
-        const int c = (((cst[e] + 1) >> 1) + (dense + 127) / 128) * pair_w(p, it, n_pairs);
-        if (it < p.full_items)
-          atomicAdd(&A[it % G], c);
-        else
-          tP[it - p.full_items] = c;
-      }
-    }
-    __syncwarp();
-    int carry = 0;
-    for (int k0 = 0; k0 < R; k0 += 32) {
-      const int k = k0 + lane;
-      const int cost = k < R ? tP[k] : 0;
-      int incl = cost;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      __syncwarp();
-      if (k < R) tP[k] = carry + incl - cost;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    const int Wt = carry;
-    int md = R <= 0 ? 0 : (Wt >= 8 * G && p.part_o ? 2 : 1);
-    if (md == 2) {
-      long long tot = 0;
-      for (int cc = lane; cc < G; cc += 32) tot += A[cc];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      tot += Wt;
-      const double target = (double)tot / G;
-      long long scar = 0;
-      for (int c0 = 0; c0 < G; c0 += 32) {
-        const int cc = c0 + lane;
-        long long sl = 0;
-        if (cc < G) {
-          const double d = target - (double)A[cc];
-          sl = d > 0.0 ? (long long)(d + 0.5) : 0;
-        }
-        long long incl = sl;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const long long v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        __syncwarp();
-        if (cc < G) A[cc] = (int)min(scar + incl - sl, (long long)INT_MAX);  // slack prefix (excl.)
-        scar += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      __syncwarp();
-      const long long S = scar > 0 ? scar : 1;
-      for (int cc = lane; cc < G; cc += 32)
-        A[cc] = scar > 0 ? (int)((long long)Wt * A[cc] / S) : (int)((long long)Wt * cc / G);
-      if (lane == 0) A[G] = Wt;
-    }
-    if (lane == 0) {
-      tP[R > 0 ? R : 0] = Wt;
-      *tail_mode = md;
-    }
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int mode = *tail_mode;
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA producer
@@ -601,23 +528,120 @@ __global__ void __launch_bounds__(384, 1)
   } else if (warp == 2) {
     // ------------------------------------------------------------- unit scheduler
     // resolves this CTA's units (global metadata loads included) ahead of the
-    // roles that consume them
-    UnitIter5 U(p, tail, mode, R, n_pairs);
-    Unit5 u;
+    // roles that consume them.  The first whole item needs no table and goes
+    // out before the tail table is built, so the pipeline starts at once.
     uint32_t qi = 0;
-    bool more = true;
-    while (more) {
-      more = U.next(u);
-      if (!more) u.item = -1;
+    auto push = [&](const Unit5& uu) {
       const int slot = qi % C::QD;
       mbar_wait(uq_empty + slot, ((qi / C::QD) & 1) ^ 1);
       if (lane == 0) {
-        uq[slot] = u;
+        uq[slot] = uu;
         mbar_arrive(uq_full + slot);  // release: the slot's contents are visible
       }
       __syncwarp();
       ++qi;
+    };
+    Unit5 u;
+    const bool first_whole = (int)blockIdx.x < p.full_items;
+    if (first_whole) {
+      UnitIter5 U0(p, tail, 0, 0, n_pairs);
+      const int T = pair_T(p, blockIdx.x);
+      U0.fill(u, blockIdx.x, T, 0, T, 1, 0, blockIdx.x, blockIdx.x, -1);
+      push(u);
     }
+    {
+      // ---- tail table.  cost(item) = key tiles x pair_w: 4 per tile for two
+      // query tiles, 3 for one (a lone query tile's softmax/MMA chain has no
+      // partner to overlap with, so it costs 3/4 of a pair's time, not 1/2).
+      // Whole items [0, full_items) go round-robin (CTA c: c, c+G, ...); the
+      // tail's cost is then shared out so that every CTA ends with about the
+      // same total: CTA c gets tail range [A[c], A[c+1]) sized by its slack
+      // under the mean load.  All item costs are fetched with 8 loads in flight
+      // per lane (one L2 round trip per 256 items).
+      int* tP = tail;
+      int* A = tail + C::MAX_TAIL + 1;
+      const int G = gridDim.x;
+      for (int cc = lane; cc <= G; cc += 32) A[cc] = 0;
+      __syncwarp();
+      for (int i0 = 0; i0 < total_items; i0 += 256) {
+        int cst[8];
+  #pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int it = i0 + e * 32 + lane;
+          cst[e] = it < total_items ? p.seg_count ? p.seg_count[it] : 0 : 0;
+        }
+  #pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int it = i0 + e * 32 + lane;
+          if (it >= total_items) continue;
+          const int dense = p.dense_hi > p.dense_lo ? p.dense_hi - p.dense_lo : 0;
+          const int c = (((cst[e] + 1) >> 1) + (dense + 127) / 128) * pair_w(p, it, n_pairs);
+          if (it < p.full_items)
+            atomicAdd(&A[it % G], c);
+          else
+            tP[it - p.full_items] = c;
+        }
+      }
+      __syncwarp();
+      int carry = 0;
+      for (int k0 = 0; k0 < R; k0 += 32) {
+        const int k = k0 + lane;
+        const int cost = k < R ? tP[k] : 0;
+        int incl = cost;
+  #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        __syncwarp();
+        if (k < R) tP[k] = carry + incl - cost;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      const int Wt = carry;
+      int md = R <= 0 ? 0 : (Wt >= 8 * G && p.part_o ? 2 : 1);
+      if (md == 2) {
+        long long tot = 0;
+        for (int cc = lane; cc < G; cc += 32) tot += A[cc];
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        tot += Wt;
+        const double target = (double)tot / G;
+        long long scar = 0;
+        for (int c0 = 0; c0 < G; c0 += 32) {
+          const int cc = c0 + lane;
+          long long sl = 0;
+          if (cc < G) {
+            const double d = target - (double)A[cc];
+            sl = d > 0.0 ? (long long)(d + 0.5) : 0;
+          }
+          long long incl = sl;
+  #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+          }
+          __syncwarp();
+          if (cc < G) A[cc] = (int)min(scar + incl - sl, (long long)INT_MAX);  // slack prefix (excl.)
+          scar += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        const long long S = scar > 0 ? scar : 1;
+        for (int cc = lane; cc < G; cc += 32)
+          A[cc] = scar > 0 ? (int)((long long)Wt * A[cc] / S) : (int)((long long)Wt * cc / G);
+        if (lane == 0) A[G] = Wt;
+      }
+      if (lane == 0) {
+        tP[R > 0 ? R : 0] = Wt;
+        *tail_mode = md;
+      }
+  
+    }
+    __syncwarp();
+    UnitIter5 U(p, tail, *tail_mode, R, n_pairs);
+    if (first_whole) U.i += gridDim.x;
+    while (U.next(u)) push(u);
+    u.item = -1;
+    push(u);
   } else if (warp >= 4) {
     // ------------------------------------------------------------- softmax + epilogue
     const int X = (warp - 4) >> 2;  // query tile of the pair
@@ -629,7 +653,14 @@ __global__ void __launch_bounds__(384, 1)
     const float c2 = p.scale_log2;
     Unit5 u;
     uint32_t ns = 0, no = 0, nu = 0, qi = 0;
+#ifdef LF_V5_TRACE
+    int st_units = 0, st_merges = 0, st_split = 0;
+#endif
     while (pop_unit(uq, uq_full, uq_empty, qi, u)) {
+#ifdef LF_V5_TRACE
+      ++st_units;
+      st_split += u.nparts > 1;
+#endif
       const int wid = u.item;
       const int nseg = u.nseg;
       const int4* segs = p.segs ? p.segs + (size_t)wid * p.seg_cap : nullptr;
@@ -687,54 +718,79 @@ __global__ void __launch_bounds__(384, 1)
         for (int g = 0; g < 8; ++g) mx[g] = fmaxf(mx[g], mx[g + 8]);
         const float mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]),
                                fmaxf(mx[6], mx[7]));
-        const float m_new = fmaxf(m_used, mt);
-        const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
-        const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
-        if (need) {
-          l *= factor;
-          m_used = m_new;
-        }
-        if (__any_sync(0xffffffffu, need) && k > 0) {
-          // O_X holds PV up to the previous tile (completed before S_X(j) was
-          // signalled); rescale it before this tile's PV is released
-#pragma unroll 1
-          for (int c = 0; c < D / 16; ++c) {
-            float o[16];
-            tmem_ld16(t_row + o_col + c * 16, o);
-            tmem_ld_wait();
+        uint64_t acc[2] = {0ull, 0ull};
+        const uint64_t c2v = f2pack(c2, c2);
+        // P = 2^(s c2 - msub) for key chunks [c0, c1) (16 keys each) -> TMEM
+        auto exps = [&](int c0, int c1, float msub) {
+          const uint64_t nm = f2pack(-msub, -msub);
 #pragma unroll
-            for (int e = 0; e < 16; ++e) o[e] *= factor;
-            tmem_st16(t_row + o_col + c * 16, reinterpret_cast<uint32_t*>(o));
+          for (int ch = c0; ch < c1; ++ch) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              float a, bb;
+              f2unpack(ffma2(f2pack(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]), c2v, nm), a, bb);
+              if (POLY > 0 && (8 * (ch & 1) + e) % POLY == POLY - 1) {
+                exp2_poly2(a, bb);
+              } else {
+                a = ex2(a);
+                bb = ex2(bb);
+              }
+              acc[e & 1] = fadd2(acc[e & 1], f2pack(a, bb));
+              pk[e] = pack_bf16(a, bb);
+            }
+            tmem_st8(t_row + s_col + 8 * ch, pk);
           }
+        };
+        auto release = [&](int hh) {  // a key half of P is in TMEM: release its PV
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(p_full + 2 * X + hh);
+          if (tr) LF_TRACE(X * 512 + (ns - 1) * 8 + 4 + hh, clk64());
+        };
+        // Row max update with lazy rescaling: O and l are rescaled only when a
+        // row max grows by more than 2^8 (P <= 2^8 is exact enough in bf16).
+        auto update_max = [&]() {
+          const float m_new = fmaxf(m_used, mt);
+          const bool need = (m_new - m_used) * c2 > 8.0f;  // false for NaN (-inf - -inf)
+          const float factor = need ? ex2((m_used - m_new) * c2) : 1.0f;
+          if (need) {
+            l *= factor;
+            m_used = m_new;
+          }
+          if (__any_sync(0xffffffffu, need) && k > 0) {
+            // O_X holds PV up to the previous tile (completed before S_X(j) was
+            // signalled); rescale it before this tile's PV is released
+#pragma unroll 1
+            for (int c = 0; c < D / 16; ++c) {
+              float o[16];
+              tmem_ld16(t_row + o_col + c * 16, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 16; ++e) o[e] *= factor;
+              tmem_st16(t_row + o_col + c * 16, reinterpret_cast<uint32_t*>(o));
+            }
+          }
+        };
+        const bool stale_ok = k > 0 && !__any_sync(0xffffffffu, m_used == -INFINITY);
+        if (stale_ok) {
+          // steady state: the first key half is exponentiated against the running
+          // max while this tile's max is reduced alongside; only if some row max
+          // grew by > 2^8 is that half redone after the rescale (rare)
+          exps(0, 4, m_used * c2);
+          if (__any_sync(0xffffffffu, (fmaxf(m_used, mt) - m_used) * c2 > 8.0f)) {
+            update_max();
+            acc[0] = acc[1] = 0ull;
+            exps(0, 4, m_used * c2);
+          }
+        } else {
+          update_max();
+          exps(0, 4, m_used == -INFINITY ? 0.f : m_used * c2);
         }
         if (tr) LF_TRACE(X * 512 + (ns - 1) * 8 + 3, clk64());
-        const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
-        const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
-        uint64_t acc[2] = {0ull, 0ull};
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {  // 16 keys (8 packed P columns) at a time
-          uint32_t pk[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            float a, bb;
-            f2unpack(ffma2(f2pack(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]), c2v, nm), a, bb);
-            if (POLY > 0 && (8 * (ch & 1) + e) % POLY == POLY - 1) {
-              exp2_poly2(a, bb);
-            } else {
-              a = ex2(a);
-              bb = ex2(bb);
-            }
-            acc[e & 1] = fadd2(acc[e & 1], f2pack(a, bb));
-            pk[e] = pack_bf16(a, bb);
-          }
-          tmem_st8(t_row + s_col + 8 * ch, pk);
-          if (ch == 3 || ch == 7) {  // a key half of P is in TMEM: release its PV
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(p_full + 2 * X + (ch >> 2));
-            if (tr) LF_TRACE(X * 512 + (ns - 1) * 8 + 4 + (ch >> 2), clk64());
-          }
-        }
+        release(0);
+        exps(4, 8, m_used == -INFINITY ? 0.f : m_used * c2);
+        release(1);
         acc[0] = fadd2(acc[0], acc[1]);
         float a, bb;
         f2unpack(acc[0], a, bb);
@@ -810,27 +866,32 @@ __global__ void __launch_bounds__(384, 1)
         ++nu;
         continue;
       }
-      // ---- split item: publish this part's unnormalised O and (m, l); the last
-      // part to finish merges all parts in CTA order (bit-reproducible).
-      // Partial layout [slot][X][D/4][128 rows] of float4: a warp's access to one
-      // column quad covers 32 consecutive rows (512 contiguous bytes).
+      // ---- split item.  Each part publishes its O normalised by its own l as
+      // fp16 (|O/l| <= max|v|) plus (m, l); the last part to finish merges.
+      // Every part enters the merge through the same fp16 round trip, so the
+      // result does not depend on which CTA merges (bit-reproducible replays).
+      // Partial layout per (slot, X): [D/8 column octets][128 rows][8 halves],
+      // i.e. 32 KB contiguous; a warp store of one octet covers 512 B.
       const int slot = blockIdx.x * 2 + (u.cfirst == (int)blockIdx.x ? 1 : 0);
-      auto part4 = [&](int sl) {
-        return reinterpret_cast<float4*>(p.part_o) + (long long)(sl * 2 + X) * (D / 4) * 128 + row;
+      auto part8 = [&](int sl) {
+        return reinterpret_cast<uint4*>(p.part_o) + (long long)(sl * 2 + X) * (D / 8) * 128;
       };
+      const float inv_own = k > 0 && l > 0.f ? 1.0f / l : 0.f;
       if (k > 0) {
-        float4* po = part4(slot);
+        uint4* po = part8(slot) + row;
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           float o[32];
           tmem_ld32(t_row + o_col + c * 32, o);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            po[(c * 8 + e) * 128] = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
+          for (int e = 0; e < 4; ++e)
+            po[(c * 4 + e) * 128] = make_uint4(
+                pack_f16(o[8 * e] * inv_own, o[8 * e + 1] * inv_own),
+                pack_f16(o[8 * e + 2] * inv_own, o[8 * e + 3] * inv_own),
+                pack_f16(o[8 * e + 4] * inv_own, o[8 * e + 5] * inv_own),
+                pack_f16(o[8 * e + 6] * inv_own, o[8 * e + 7] * inv_own));
         }
-        tc_fence_before();
-        mbar_arrive(o_empty + X);
       }
       p.part_ml[(long long)slot * 256 + X * 128 + row] = make_float2(m_used, k > 0 ? l : 0.f);
       if (tru) LF_TRACE(X * 512 + 460 + nu * 4, clk64());
@@ -847,61 +908,86 @@ __global__ void __launch_bounds__(384, 1)
       if (tru) LF_TRACE(X * 512 + 460 + nu * 4 + 1, clk64());
       if (tru) LF_TRACE(X * 512 + 460 + nu * 4 + 3, last ? 1 : 2);
       ++nu;
+      if (k > 0) {  // O_X was published: the next unit's first PV may overwrite it
+        tc_fence_before();
+        mbar_arrive(o_empty + X);
+      }
       if (!last) {
         release_q();
         continue;
       }
       __threadfence();
+#ifdef LF_V5_TRACE
+      ++st_merges;
+#endif
       const bool trm = tru && nu == 1;
       if (trm) LF_TRACE(X * 512 + 480, clk64());
-      // parts: the CTAs of [cfirst, clast] with non-empty tail ranges, in order
       const int* A = tail + C::MAX_TAIL + 1;
+      auto next_part = [&](int cc) {
+        while (cc <= u.clast && A[cc + 1] <= A[cc]) ++cc;
+        return cc;
+      };
+      auto slot_of = [&](int cc) { return cc * 2 + (cc == u.cfirst); };
       float M = -INFINITY;
-      for (int cc = u.cfirst; cc <= u.clast; ++cc) {
-        if (A[cc + 1] <= A[cc]) continue;
-        const float2 ml = __ldcg(&p.part_ml[(long long)(cc * 2 + (cc == u.cfirst)) * 256 + X * 128 + row]);
+      for (int cc = next_part(u.cfirst); cc <= u.clast; cc = next_part(cc + 1)) {
+        const float2 ml = __ldcg(&p.part_ml[(long long)slot_of(cc) * 256 + X * 128 + row]);
         if (ml.y > 0.f) M = fmaxf(M, ml.x);
       }
+      // weight of part cc in the merge: l_cc 2^((m_cc - M) c2)
+      auto weight = [&](int cc) {
+        const float2 ml = __ldcg(&p.part_ml[(long long)slot_of(cc) * 256 + X * 128 + row]);
+        return (ml.y > 0.f && ml.x != -INFINITY) ? ml.y * ex2((ml.x - M) * c2) : 0.f;
+      };
       float L = 0.f;
-      for (int cc = u.cfirst; cc <= u.clast; ++cc) {
-        if (A[cc + 1] <= A[cc]) continue;
-        const float2 ml = __ldcg(&p.part_ml[(long long)(cc * 2 + (cc == u.cfirst)) * 256 + X * 128 + row]);
-        if (ml.y > 0.f && ml.x != -INFINITY) L += ml.y * ex2((ml.x - M) * c2);
-      }
+      for (int cc = next_part(u.cfirst); cc <= u.clast; cc = next_part(cc + 1)) L += weight(cc);
       if (row_ok && !(L > 0.f) && p.err) atomicOr(p.err, 1);
       const float inv = 1.0f / L;
       if (trm) LF_TRACE(X * 512 + 481, clk64());
-      // 32-column quarters; a part with l = 0 never wrote its O, so its stale
-      // values must not reach the sum (not even as 0 * inf)
-      constexpr int QC = 32;
+      // parts in CTA order, all of a part's octet loads in flight together
+      // (a part with l = 0 never wrote its O: skipped, stale values never read)
 #pragma unroll 1
-      for (int hf = 0; hf < D / QC; ++hf) {
-        float acc[QC];
+      for (int hf = 0; hf < 2; ++hf) {
+        float acc[D / 2];
 #pragma unroll
-        for (int e = 0; e < QC; ++e) acc[e] = 0.f;
-        for (int cc = u.cfirst; cc <= u.clast; ++cc) {
-          if (A[cc + 1] <= A[cc]) continue;
-          const int sl = cc * 2 + (cc == u.cfirst);
-          const float2 ml = __ldcg(&p.part_ml[(long long)sl * 256 + X * 128 + row]);
-          const float4* src = part4(sl) + hf * (QC / 4) * 128;
-          float4 x4[QC / 4];
+        for (int e = 0; e < D / 2; ++e) acc[e] = 0.f;
+        // two parts per round, loads issued unconditionally (a part with l = 0
+        // contributes through a select, so its stale values never reach acc)
+        for (int ca = next_part(u.cfirst); ca <= u.clast;) {
+          const int cb = next_part(ca + 1);
+          const bool two = cb <= u.clast;
+          const float wa = weight(ca), wb = two ? weight(cb) : 0.f;
+          const uint4* pa = part8(slot_of(ca)) + (hf * (D / 16)) * 128 + row;
+          const uint4* pb = part8(slot_of(two ? cb : ca)) + (hf * (D / 16)) * 128 + row;
+          uint4 xa[D / 16], xb[D / 16];
 #pragma unroll
-          for (int e = 0; e < QC / 4; ++e) x4[e] = __ldcg(src + e * 128);
-          const float f = (ml.y > 0.f && ml.x != -INFINITY) ? ex2((ml.x - M) * c2) : 0.f;
-          if (f != 0.f) {
+          for (int e = 0; e < D / 16; ++e) {
+            xa[e] = __ldcg(pa + e * 128);
+            xb[e] = __ldcg(pb + e * 128);
+          }
 #pragma unroll
-            for (int e = 0; e < QC / 4; ++e) {
-              acc[4 * e] += x4[e].x * f; acc[4 * e + 1] += x4[e].y * f;
-              acc[4 * e + 2] += x4[e].z * f; acc[4 * e + 3] += x4[e].w * f;
+          for (int e = 0; e < D / 16; ++e) {
+            const uint32_t ha[4] = {xa[e].x, xa[e].y, xa[e].z, xa[e].w};
+            const uint32_t hb[4] = {xb[e].x, xb[e].y, xb[e].z, xb[e].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float a0, a1, b0, b1;
+              unpack_f16(ha[q], a0, a1);
+              unpack_f16(hb[q], b0, b1);
+              acc[8 * e + 2 * q] += (wa != 0.f ? a0 * wa : 0.f);
+              acc[8 * e + 2 * q + 1] += (wa != 0.f ? a1 * wa : 0.f);
+              acc[8 * e + 2 * q] += (wb != 0.f ? b0 * wb : 0.f);
+              acc[8 * e + 2 * q + 1] += (wb != 0.f ? b1 * wb : 0.f);
             }
           }
+          ca = two ? next_part(cb + 1) : cb;
         }
+        if (hf == 0 && trm) LF_TRACE(X * 512 + 482, clk64());
 #pragma unroll
-        for (int c = 0; c < QC / 16; ++c) {
+        for (int c = 0; c < D / 32; ++c) {
           if (use_tma)
-            stage16(hf * QC + 16 * c, acc + 16 * c, inv);
+            stage16(hf * (D / 2) + 16 * c, acc + 16 * c, inv);
           else if (row_ok)
-            store_row<D, 16>(p, u.h, grow, hf * QC + 16 * c, acc + 16 * c, inv);
+            store_row<D, 16>(p, u.h, grow, hf * (D / 2) + 16 * c, acc + 16 * c, inv);
         }
       }
       if (use_tma) tma_store_rows();
@@ -911,8 +997,20 @@ __global__ void __launch_bounds__(384, 1)
         p.lse[(long long)u.h * p.Lq + grow] = (M == -INFINITY ? -INFINITY : M * p.scale) + logf(L);
       if (tru) LF_TRACE(X * 512 + 460 + (nu - 1) * 4 + 2, clk64());
     }
+#ifdef LF_V5_TRACE
+    st_units_g = st_units;
+    st_merges_g = st_merges;
+    st_split_g = st_split;
+#endif
   }
   if (warp >= 4 && lane == 0) bulk_wait_all();  // TMA output stores complete
+#ifdef LF_V5_TRACE
+  if ((p.debug & 255) == 2 && p.trace && threadIdx.x == 128) {
+    p.trace[2048 + 4 * blockIdx.x] = st_units_g;
+    p.trace[2049 + 4 * blockIdx.x] = st_merges_g;
+    p.trace[2050 + 4 * blockIdx.x] = st_split_g;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

@@ -160,13 +160,24 @@ int launch_pool(PoolArgs& a, int dtype, int vec, int ns, cudaStream_t st) {
                           : launch_pool_t<float>(a, vec, ns, st);
 }
 
-// attention kernel generation: 5 (default; query-tile pairs, 256-row plans)
-// or 3 (legacy single-tile kernel, 128-row plans), LF_ATTN_VER overrides
+// forced attention kernel (LF_ATTN_VER=3|5, for experiments), 0 = per call
 int attn_ver() {
-  static const int v = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 3;
-  return v == 3 ? 3 : 5;
+  static const int v = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 0;
+  return v == 3 || v == 5 ? v : 0;
 }
-int plan_rows() { return attn_ver() == 5 ? 2 * kTileRows : kTileRows; }
+
+// Work-based kernel choice: the pair kernel is faster per key tile (two query
+// tiles share each K/V tile and ping-pong softmax against the tensor core) but
+// pays a unit-boundary and stream-K merge overhead per CTA that only long work
+// amortises (measured on B200: tile kernel ahead below ~100 pair-steps per SM).
+int choose_kernel(int heads, int n_qtiles, int dense_keys, int past_tiles, int sms) {
+  const long long n_pairs = (n_qtiles + 1) / 2;
+  const long long steps = n_pairs * heads * ((dense_keys + 127) / 128 + (past_tiles > 0 ? past_tiles : 0));
+  return steps >= 100LL * sms ? LF_KERNEL_PAIR : LF_KERNEL_TILE;
+}
+// tile plans cover query-tile pairs (256 rows) for both kernels (the tile
+// kernel skips the key tiles only its partner tile needs)
+int plan_rows() { return 2 * kTileRows; }
 
 int max_qblocks_per_tile(lf_tiling qt, int rows = kTileRows) {
   Tiling t(qt);
@@ -251,18 +262,18 @@ int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
   if ((p.debug & 255) == 2) {
     static long long* tr = nullptr;
     if (!tr) {
-      cudaMalloc(&tr, 2048 * 8);
-      cudaMemset(tr, 0, 2048 * 8);
+      cudaMalloc(&tr, 4096 * 8);
+      cudaMemset(tr, 0, 4096 * 8);
     }
     p.trace = tr;
     static int dumps = 0;
     if (dumps++ == 3) {  // dump after a few launches (ordered with the stream)
       cudaStreamSynchronize(S(stream));
-      static long long h[2048];
+      static long long h[4096];
       cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
       FILE* f = fopen("gpurun_out/attn_trace.txt", "w");
       if (f) {
-        for (int i = 0; i < 2048; ++i) fprintf(f, "%lld\n", h[i]);
+        for (int i = 0; i < 4096; ++i) fprintf(f, "%lld\n", h[i]);
         fclose(f);
       }
     }
@@ -359,6 +370,23 @@ int hsa_geom(const lf_hsa_args* a, HsaGeom* g) {
   return LF_OK;
 }
 
+// Non-dense key tiles per 256-row plan tile, from the host copy of s_i: each
+// query block keeps <= min(budget, topk*bpf) past blocks, a plan tile unions
+// its <= mq query blocks' lists (bounded by all past blocks).  -1: unknown.
+int past_tiles_estimate(const lf_hsa_args* a, const HsaGeom& g) {
+  const double s = a->s_i_host;
+  if (!(s >= 0.0 && s < 1.0) || g.P <= 0) return g.P <= 0 ? 0 : -1;
+  const int cur = a->f * g.bpf;
+  const long long total = (long long)((1.0 - s) * a->chunk_index * cur + 0.5);
+  long long past = total - cur;
+  if (past <= 0) return 0;
+  past = past < g.cap ? past : g.cap;
+  const long long mq = max_qblocks_per_tile(g.qt, plan_rows());
+  long long blocks = mq * past;
+  blocks = blocks < g.list_blocks ? blocks : g.list_blocks;
+  return (int)((blocks + 1) / 2);
+}
+
 struct HsaWs {
   float *q_block, *k_block, *k_frame;
   int *blocks, *count, *frames, *budget, *seg_count;
@@ -395,6 +423,18 @@ extern "C" {
 int lf_version(void) { return 100; }
 
 int lf_plan_tile_rows(void) { return plan_rows(); }
+
+int lf_attention_kernel_choice(int32_t heads, int32_t q_rows, int32_t dense_keys,
+                               int32_t past_tiles_hint) {
+  if (attn_ver()) return attn_ver();
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  return choose_kernel(heads, (q_rows + 127) / 128, dense_keys, past_tiles_hint, sms);
+}
 
 const char* lf_strerror(int status) {
   switch (status) {
@@ -605,6 +645,17 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
                  int32_t dense_lo, int32_t dense_hi, float scale, void* out, int32_t out_dtype,
                  int64_t out_row_stride, int64_t out_head_stride, float* lse, int32_t* err_flag,
                  void* stream) {
+  return lf_attention_ex(q, k, v, q_tiling, segs, seg_count, seg_cap, dense_lo, dense_hi, scale,
+                         out, out_dtype, out_row_stride, out_head_stride, lse, err_flag,
+                         LF_KERNEL_AUTO, -1, stream);
+}
+
+int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                    const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                    int32_t dense_lo, int32_t dense_hi, float scale, void* out,
+                    int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
+                    float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
+                    void* stream) {
   int rc;
   if ((rc = check_mat(q, "q")) || (rc = check_mat(k, "k")) || (rc = check_mat(v, "v"))) return rc;
   if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
@@ -650,7 +701,12 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  if (attn_ver() == 5) {
+  p.plan_pairs = plan_rows() != kTileRows;
+  if (kernel != LF_KERNEL_TILE && kernel != LF_KERNEL_PAIR)
+    kernel = choose_kernel(q->heads, p.n_qtiles, dense_hi > dense_lo ? dense_hi - dense_lo : 0,
+                           past_tiles_hint, sms);
+  if (attn_ver()) kernel = attn_ver();
+  if (kernel == LF_KERNEL_PAIR) {
     p.tma_out = out_dtype == LF_BF16 && !getenv("LF_ATTN_NO_TMA_OUT") &&
                 make_out_map(&p.to, out, q->d, q->rows, q->heads, out_row_stride, out_head_stride);
     return launch_v5(p, q->heads, q->d, sms, stream);
@@ -705,10 +761,11 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
     return rc;
   lf_mat kk = a->k, vv = a->v;
   kk.rows = vv.rows = a->chunk_index * a->f * a->n;
-  return lf_attention(&a->q, &kk, &vv, g.qt, reinterpret_cast<const int32_t*>(w.segs), w.seg_count,
-                      g.seg_cap, g.dense_lo, g.dense_hi, 1.0f / sqrtf((float)g.d), a->out,
-                      a->out_dtype, a->out_row_stride, a->out_head_stride, a->lse, a->err_flag,
-                      stream);
+  return lf_attention_ex(&a->q, &kk, &vv, g.qt, reinterpret_cast<const int32_t*>(w.segs),
+                         w.seg_count, g.seg_cap, g.dense_lo, g.dense_hi,
+                         1.0f / sqrtf((float)g.d), a->out, a->out_dtype, a->out_row_stride,
+                         a->out_head_stride, a->lse, a->err_flag, a->attn_kernel,
+                         past_tiles_estimate(a, g), stream);
 }
 
 int lf_rowdot(const float* A, int32_t rows, int32_t d, const float* x, double* out, void* stream) {

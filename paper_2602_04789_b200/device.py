@@ -195,10 +195,31 @@ def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
     return TilePlan(segs, seg_count, seg_cap)
 
 
+def past_tiles_hint(s_host, chunk: int, f: int, bpf: int, topk_frames: int,
+                    qt: TilingSpec) -> int:
+    """Estimated non-dense 128-key tiles per 256-row plan tile (the work hint of
+    lf_attention_ex; mirrors past_tiles_estimate in lfattn.cu).  -1 if unknown."""
+    P = (chunk - 1) * f
+    if P <= 0:
+        return 0
+    if s_host is None or not (0.0 <= float(s_host) < 1.0):
+        return -1
+    cur = f * bpf
+    past = int((1.0 - float(s_host)) * chunk * cur + 0.5) - cur
+    if past <= 0:
+        return 0
+    past = min(past, min(topk_frames, P) * bpf)
+    blocks = min(qt.max_blocks_per_tile(plan_rows()) * past, P * bpf)
+    return (blocks + 1) // 2
+
+
 def attention(q, k, v, qt: TilingSpec, tiles: TilePlan | None, dense_lo: int, dense_hi: int,
               out: torch.Tensor | None = None, out_dtype=torch.float32, scale: float | None = None,
-              lse: torch.Tensor | None = None, err: torch.Tensor | None = None) -> torch.Tensor:
-    """Block-sparse flash attention over bf16 [H, L, d] (d in {64, 128})."""
+              lse: torch.Tensor | None = None, err: torch.Tensor | None = None,
+              kernel: int = L.LF_KERNEL_AUTO, past_tiles: int = -1) -> torch.Tensor:
+    """Block-sparse flash attention over bf16 [H, L, d] (d in {64, 128}).
+
+    kernel / past_tiles: lf_attention_ex's kernel choice and work hint."""
     lib = L.lib()
     H, Lq, d = q.shape
     if out is None:
@@ -207,12 +228,13 @@ def attention(q, k, v, qt: TilingSpec, tiles: TilePlan | None, dense_lo: int, de
     mq, mk, mv = L.mat(q), L.mat(k), L.mat(v)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
-    L.check(lib.lf_attention(ctypes.byref(mq), ctypes.byref(mk), ctypes.byref(mv), qt.abi(),
-                             tiles.segs.data_ptr() if tiles else None,
-                             tiles.seg_count.data_ptr() if tiles else None,
-                             tiles.seg_cap if tiles else 0, int(dense_lo), int(dense_hi),
-                             float(scale), out.data_ptr(), odt, out.stride(1), out.stride(0),
-                             L.ptr(lse), L.ptr(err), L.stream_ptr()))
+    L.check(lib.lf_attention_ex(ctypes.byref(mq), ctypes.byref(mk), ctypes.byref(mv), qt.abi(),
+                                tiles.segs.data_ptr() if tiles else None,
+                                tiles.seg_count.data_ptr() if tiles else None,
+                                tiles.seg_cap if tiles else 0, int(dense_lo), int(dense_hi),
+                                float(scale), out.data_ptr(), odt, out.stride(1), out.stride(0),
+                                L.ptr(lse), L.ptr(err), int(kernel), int(past_tiles),
+                                L.stream_ptr()))
     return out
 
 

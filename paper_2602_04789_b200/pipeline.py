@@ -44,6 +44,8 @@ class HsaPipeline:
         self._graph = None
         self._bound = None
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.attn_kernel = L.LF_KERNEL_AUTO
+        self._s_host = None
 
     # ------------------------------------------------------------------ binding
     def _make_args(self, q, k, v, s_dev, out):
@@ -62,10 +64,15 @@ class HsaPipeline:
         a.out_head_stride = out.stride(0)
         a.lse = None
         a.err_flag = self.err.data_ptr()
+        a.attn_kernel = self.attn_kernel
+        a.s_i_host = float("nan") if self._s_host is None else float(self._s_host)
         return a
 
-    def bind(self, q, k, v, s_i, out=None):
-        """Fix the buffers a (captured) call reads and writes."""
+    def bind(self, q, k, v, s_i, out=None, s_host=None):
+        """Fix the buffers a (captured) call reads and writes.
+
+        s_host: host value of s_i when s_i is a device tensor (the kernel choice
+        uses it; None = unknown)."""
         lib = L.lib()
         H, d = self.heads, self.layout.d
         for name, t, rows in (("q", q, self.lq), ("k", k, self.lk), ("v", v, self.lk)):
@@ -73,7 +80,9 @@ class HsaPipeline:
                 raise ValueError(f"{name}: expected bf16 [{H}, L, {d}], got {t.dtype} {tuple(t.shape)}")
             if t.shape[1] < rows:
                 raise ValueError(f"{name}: {t.shape[1]} rows < {rows}")
+        self._s_host = s_host
         if not torch.is_tensor(s_i):
+            self._s_host = float(s_i)
             s_i = torch.tensor([float(s_i)], dtype=torch.float64, device=self.device)
         if out is None:
             out = torch.empty((H, self.lq, d), dtype=self.out_dtype, device=self.device)

@@ -135,7 +135,7 @@ class HsaRollout:
                                    L.stream_ptr()))
 
     def step(self, q: torch.Tensor, k_cur: torch.Tensor, v_cur: torch.Tensor, chunk_index: int,
-             s_i=None, out: torch.Tensor | None = None) -> torch.Tensor:
+             s_i=None, out: torch.Tensor | None = None, s_host=None) -> torch.Tensor:
         """One denoising step of chunk i (rollout.py:254-273 attention part).
 
         q, k_cur, v_cur: bf16 [H, f*n, d] for the noisy current chunk.
@@ -161,6 +161,11 @@ class HsaRollout:
         lk = lay.context_tokens(i)
         self.last_selection = sel
         self.last_chunk = i
+        if s_host is None and s_i is not None and not torch.is_tensor(s_i):
+            s_host = float(s_i)
+        if s_host is None and s_i is None and self.plan is not None:
+            s_host = float(self.plan.s[i - 1])
+        hint = D.past_tiles_hint(s_host, i, lay.f, self.bpf, self.cfg.topk_frames, qt)
         return D.attention(q, self.kv_k[:, :lk], self.kv_v[:, :lk], qt, tiles, P * lay.n, lk,
                            out=out, out_dtype=self.out_dtype, scale=1.0 / math.sqrt(lay.d),
-                           err=self.err)
+                           err=self.err, past_tiles=hint)
