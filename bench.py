@@ -97,7 +97,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
-                 "200", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "50", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
         except OSError:
             return self
@@ -426,24 +426,21 @@ def run_ours(args, c):
             gs.append(g)
         graphs.append(gs)
     torch.cuda.synchronize()
+    # each stage's graphs replayed back to back (T different inputs in rotation,
+    # > L2 in total) between two events on this stream: per-launch device time
+    # with the host launch latency of the graph hidden behind the previous replay
     reps = max(5, min(args.steps, 50))
-    evs = []
-    for r in range(reps):
-        for s in range(T):
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            ev[0].record()
-            graphs[s][0].replay()
-            ev[1].record()
-            graphs[s][1].replay()
-            ev[2].record()
-            graphs[s][2].replay()
-            ev[3].record()
-            evs.append(ev)
-    torch.cuda.synchronize()
-    for ev in evs:
-        stage["pool"].append(ev[0].elapsed_time(ev[1]))
-        stage["select"].append(ev[1].elapsed_time(ev[2]))
-        stage["attn"].append(ev[2].elapsed_time(ev[3]))
+    for si, name in enumerate(("pool", "select", "attn")):
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for s in range(T):  # warm
+            graphs[s][si].replay()
+        ea.record()
+        for r in range(reps):
+            for s in range(T):
+                graphs[s][si].replay()
+        eb.record()
+        torch.cuda.synchronize()
+        stage[name].append(ea.elapsed_time(eb) / (reps * T))
     attn_ms = statistics.mean(stage["attn"])
     pool_ms = statistics.mean(stage["pool"])
     sel_ms = statistics.mean(stage["select"])
@@ -518,34 +515,89 @@ def run_ours(args, c):
     hro = [torch.empty(r_out[s].shape, dtype=r_out[s].dtype).pin_memory() for s in range(T)]
     h2d = sum(x.numel() * 2 for x in hq + hkc + hvc) + (2 * hkp.numel() * 2 if i > 1 else 0)
 
+    # copies overlap compute: H2D of step s+1 into a staging pair on a copy
+    # stream while step s runs, a device copy into the cache slot (HBM, ~10 us),
+    # D2H of each output on a third stream; PCIe H2D is the e2e bound
+    cur = torch.cuda.current_stream()
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    stg_q = [torch.empty_like(Q[0]) for _ in range(2)]
+    stg_k = [torch.empty_like(Kc[0]) for _ in range(2)]
+    stg_v = [torch.empty_like(Vc[0]) for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(T)]
+
     def e2e_rollout():
+        def h2d(s):
+            b = s & 1
+            with torch.cuda.stream(s_h2d):
+                s_h2d.wait_event(ev_free[b])  # staging b no longer read by compute
+                stg_q[b].copy_(hq[s], non_blocking=True)
+                stg_k[b].copy_(hkc[s], non_blocking=True)
+                stg_v[b].copy_(hvc[s], non_blocking=True)
+                ev_in[b].record(s_h2d)
+        h2d(0)
         if i > 1:
-            kp, vp = ro.kv_slot(i - 1)  # H2D straight into the cache slot
-            kp.copy_(hkp, non_blocking=True)
-            vp.copy_(hvp, non_blocking=True)
+            kp, vp = ro.kv_slot(i - 1)  # previous clean chunk straight into its slot
+            with torch.cuda.stream(s_h2d):
+                kp.copy_(hkp, non_blocking=True)
+                vp.copy_(hvp, non_blocking=True)
+                ev_prev = torch.cuda.Event()
+                ev_prev.record(s_h2d)
+            cur.wait_event(ev_prev)
             ro.commit(None, None, i - 1, overwrite=True)
         for s in range(T):
-            Q[s].copy_(hq[s], non_blocking=True)
+            b = s & 1
+            if s + 1 < T:
+                h2d(s + 1)
+            cur.wait_event(ev_in[b])
             kc, vc = ro.kv_slot(i)
-            kc.copy_(hkc[s], non_blocking=True)
-            vc.copy_(hvc[s], non_blocking=True)
-            ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s], s_host=s_host)
+            kc.copy_(stg_k[b])
+            vc.copy_(stg_v[b])
+            ro.step(stg_q[b], None, None, i, s_i=s_dev, out=r_out[s], s_host=s_host)
+            ev_free[b].record(cur)
             if mode == "headshard":
                 gather_heads(r_out[s], shard, out=full[s])
-            hro[s].copy_(r_out[s], non_blocking=True)
+            ev_out[s].record(cur)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev_out[s])
+                hro[s].copy_(r_out[s], non_blocking=True)
+        cur.wait_stream(s_d2h)  # the step ends when its outputs are on the host
 
     e2e_ms = timed(e2e_rollout, e2e_steps)
 
-    # ---- CPU baseline (rank 0, N = 1 only): oracle on a bounded sample of the same workload
+    # ---- CPU baseline (rank 0, N = 1 only): the oracle on a bounded sample of
+    # the same workload -- head-calls of this chunk until ~10 s of CPU work or
+    # the whole chunk (H heads x T calls), whichever comes first
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        dt, cflops = oracle_sample(c, s_host, 4242, threads)
-        cpu = {"value": cflops / dt / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": (f"1 head x 1 denoising-step call of chunk {i} (framewise oracle port "
-                          f"of chunkattn.hsa_attention), {dt:.2f} s; OPENBLAS_NUM_THREADS=1, "
-                          f"threads={threads}"),
-               "ms_per_chunk_extrapolated": dt * H * T * 1e3, "cpu": cpu_desc()}
+        tot_t, tot_f, calls = 0.0, 0, 0
+        while calls < H * T and tot_t < 10.0:
+            dt, cflops = oracle_sample(c, s_host, 4242 + calls, threads)
+            tot_t += dt
+            tot_f += cflops
+            calls += 1
+        cpu = {"value": tot_f / tot_t / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": (f"{calls} of the {H * T} head-calls of one chunk-{i} step (framewise "
+                          f"oracle port of chunkattn.hsa_attention), {tot_t:.1f} s; "
+                          f"OPENBLAS_NUM_THREADS=1, threads={threads}"),
+               "ms_per_chunk": tot_t / calls * H * T * 1e3,
+               "ms_per_chunk_is_extrapolated": calls < H * T, "cpu": cpu_desc()}
+
+    # PCIe bound of the e2e leg: the step's H2D copies alone (same pinned
+    # buffers, same order), timed on the device
+    def h2d_only():
+        if i > 1:
+            kp, vp = ro.kv_slot(i - 1)
+            kp.copy_(hkp, non_blocking=True)
+            vp.copy_(hvp, non_blocking=True)
+        for s in range(T):
+            stg_q[s & 1].copy_(hq[s], non_blocking=True)
+            stg_k[s & 1].copy_(hkc[s], non_blocking=True)
+            stg_v[s & 1].copy_(hvc[s], non_blocking=True)
+    h2d_only_ms = timed(h2d_only, 3)
+    h2d_gbs = h2d / (h2d_only_ms * 1e-3) / 1e9
 
     # pool(Q+K), pool(k_frame), select, plan_tiles, attention; chunk 1 has no past stages
     # rollout flow per chunk: commit (2 pool launches) + T x (pool Q, select,
@@ -567,7 +619,9 @@ def run_ours(args, c):
                              f"{2 * h_local * lk * d * 2 / 1e6:.0f} MB)"},
             "e2e": {"value": flops_r_step / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                     "ms_per_chunk": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "HsaRollout.commit + HsaRollout.step (C ABI underneath)"},
+                    "api": "HsaRollout.commit + HsaRollout.step (C ABI underneath); H2D / compute / D2H on three streams",
+                    "h2d_gbs_measured": h2d_gbs,
+                    "pcie_bound_ms_per_chunk": h2d_only_ms},
             "stateless": {"value": value_stateless, "unit": UNIT, "ms_per_chunk": ms_step,
                           "api": "HsaPipeline / lf_hsa_forward, full K/V per call",
                           "e2e_value": flops_step / (e2e_ms_sl * 1e-3) / 1e12,

@@ -501,6 +501,23 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
       fa.q_block = q_block; fa.k_block = k_block; fa.k_frame = k_frame;
       const int smem = per * d * 4;
       const int grid = q->heads * (fa.q_frames + fa.k_frames);
+      // contiguous rows: TMA-staged variant (bulk copies of whole blocks)
+      if ((d == 128 || d == 64) && q->row_stride == d && k->row_stride == d && q_tiling.block <= 64 &&
+          !getenv("LF_POOL_NO_TMA")) {
+        const int tsmem = (d == 128 ? PoolTmaCfg<128>::NST * PoolTmaCfg<128>::STAGE
+                                    : PoolTmaCfg<64>::NST * PoolTmaCfg<64>::STAGE) +
+                          2 * 8 * 4 + smem;
+        if (d == 128) {
+          cudaFuncSetAttribute(pool_frames_tma_kernel<128>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+          pool_frames_tma_kernel<128><<<grid, PoolTmaCfg<128>::THREADS, tsmem, S(stream)>>>(fa);
+        } else {
+          cudaFuncSetAttribute(pool_frames_tma_kernel<64>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+          pool_frames_tma_kernel<64><<<grid, PoolTmaCfg<64>::THREADS, tsmem, S(stream)>>>(fa);
+        }
+        return check_launch("pool_frames_tma_kernel");
+      }
 #define LF_FP(L)                                                                              \
   if (lpb == L) {                                                                             \
     if (smem > 48 * 1024)                                                                     \

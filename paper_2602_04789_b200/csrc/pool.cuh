@@ -265,3 +265,116 @@ __global__ void __launch_bounds__(512) pool_frames_bf16_kernel(FramePoolArgs a) 
 }
 
 }  // namespace lf
+
+namespace lf {
+
+// both bf16 halves of w as fp64 scaled by 2^-896, with integer ops only (no
+// conversion-unit traffic); exact, and fp64 sums of them round exactly like
+// the unscaled sums (power-of-two scaling, far from the subnormal range)
+__device__ __forceinline__ double bf16_lo_scaled(uint32_t w) {
+  const uint32_t hi = ((w << 16) & 0x80000000u) | ((w << 13) & 0x0FFFE000u);
+  return __hiloint2double((int)hi, 0);
+}
+
+// K1 with TMA staging: one CTA per (head, frame) streams the frame's blocks
+// (rows contiguous: row stride == d) through a 4-stage shared-memory ring with
+// cp.async.bulk; two consumer groups (even / odd blocks) sum each column in
+// fp64 in row order (bit-exact with NumPy's sequential reduction), the block
+// means go out as fp32 and, for past key frames, feed k_frame = mean of the
+// frame's block means in block order (selection.py:109-113).
+template <int D>
+struct PoolTmaCfg {
+  static constexpr int ROWS = 64;                    // block rows (b <= 64)
+  static constexpr int STAGE = ROWS * D * 2;         // bytes
+  static constexpr int NST = 4;
+  static constexpr int THREADS = 32 + D;             // producer warp + 2 groups x D/2 threads (2 cols each)
+};
+
+template <int D>
+__global__ void __launch_bounds__(PoolTmaCfg<D>::THREADS) pool_frames_tma_kernel(FramePoolArgs a) {
+  using C = PoolTmaCfg<D>;
+  extern __shared__ __align__(128) unsigned char pt_smem[];
+  unsigned char* ring = pt_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(pt_smem + C::NST * C::STAGE);
+  uint64_t* empty = full + C::NST;
+  float* fp_smem = reinterpret_cast<float*>(empty + C::NST);  // [per_period][D]
+  const int nfr = a.q_frames + a.k_frames;
+  const int h = blockIdx.x / nfr;
+  const int fr = blockIdx.x - h * nfr;
+  const bool is_q = fr < a.q_frames;
+  const int frame = is_q ? fr : fr - a.q_frames;
+  const __nv_bfloat16* base = is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
+  float* out = is_q ? a.q_block + ((long long)h * a.q_frames * a.per_period) * D
+                    : a.k_block + ((long long)h * a.k_frames * a.per_period) * D;
+  const bool keep = !is_q && frame < a.past_frames;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, D / 64);  // one arrive per consumer warp of the group
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int fe = frame * a.period + a.period;
+  if (warp == 0) {
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < a.per_period; ++j) {
+        const int r0 = frame * a.period + j * a.block;
+        int r1 = r0 + a.block;
+        r1 = r1 < fe ? r1 : fe;
+        const int st = j % C::NST;
+        const uint32_t bytes = (uint32_t)(r1 - r0) * D * 2;
+        mbar_wait(empty + st, ((j / C::NST) & 1) ^ 1);
+        mbar_expect_tx(full + st, bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(ring + st * C::STAGE)),
+            "l"(base + (long long)r0 * D), "r"(bytes), "r"(smem_u32(full + st))
+            : "memory");
+      }
+    }
+    return;
+  }
+  const int t = threadIdx.x - 32;
+  const int grp = t / (D / 2);        // 0: even blocks, 1: odd blocks
+  const int col = (t % (D / 2)) * 2;  // this thread's column pair
+  for (int j = grp; j < a.per_period; j += 2) {
+    const int r0 = frame * a.period + j * a.block;
+    int r1 = r0 + a.block;
+    r1 = r1 < fe ? r1 : fe;
+    const int st = j % C::NST;
+    mbar_wait(full + st, (j / C::NST) & 1);
+    const uint32_t* rows = reinterpret_cast<const uint32_t*>(ring + st * C::STAGE) + col / 2;
+    const int n = r1 - r0;
+    double a0 = 0.0, a1 = 0.0;
+    {
+      const uint32_t w = rows[0];
+      a0 = bf16_lo_scaled(w);
+      a1 = bf16_hi_scaled(w);
+    }
+#pragma unroll 8
+    for (int r = 1; r < n; ++r) {
+      const uint32_t w = rows[r * (D / 2)];
+      a0 += bf16_lo_scaled(w);
+      a1 += bf16_hi_scaled(w);
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(empty + st);
+    const double unscale = 0x1p896, cnt = (double)n;
+    const float m0 = (float)(a0 * unscale / cnt), m1 = (float)(a1 * unscale / cnt);
+    *reinterpret_cast<float2*>(out + ((long long)frame * a.per_period + j) * D + col) =
+        make_float2(m0, m1);
+    if (keep) *reinterpret_cast<float2*>(fp_smem + j * D + col) = make_float2(m0, m1);
+  }
+  if (!keep) return;
+  asm volatile("bar.sync 1, %0;" ::"r"(D) : "memory");  // consumer threads only
+  float* kf = a.k_frame + ((long long)h * a.past_frames + frame) * D;
+  for (int cc = t; cc < D; cc += D) {
+    double s = (double)fp_smem[cc];
+    for (int j = 1; j < a.per_period; ++j) s += (double)fp_smem[j * D + cc];
+    kf[cc] = (float)(s / (double)a.per_period);
+  }
+}
+
+}  // namespace lf

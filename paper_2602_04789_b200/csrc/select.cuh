@@ -53,6 +53,36 @@ __device__ __forceinline__ double dot_f32_dd(const float* __restrict__ row, cons
   return dd_value(acc);
 }
 
+// four dot_f32_dd at once (same per-row summation order, interleaved chains)
+__device__ __forceinline__ void dot4_f32_dd(const float* const* rows, const float* qv, int d,
+                                            double* out) {
+  DD acc[4] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  bool vec = (d & 3) == 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) vec = vec && ((reinterpret_cast<uintptr_t>(rows[u]) & 15) == 0);
+  if (vec) {
+    for (int c = 0; c < d; c += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(rows[u] + c));
+      const double q0 = qv[c], q1 = qv[c + 1], q2 = qv[c + 2], q3 = qv[c + 3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dd_add(acc[u], (double)x[u].x * q0);
+        dd_add(acc[u], (double)x[u].y * q1);
+        dd_add(acc[u], (double)x[u].z * q2);
+        dd_add(acc[u], (double)x[u].w * q3);
+      }
+    }
+  } else {
+    for (int c = 0; c < d; ++c)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dd_add(acc[u], (double)__ldg(rows[u] + c) * (double)qv[c]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) out[u] = dd_value(acc[u]);
+}
+
 // rank of element i among n scores under (-score, index) order
 __device__ __forceinline__ int stable_rank(const double* sc, int lo, int n, int i) {
   const double si = sc[i];
@@ -130,16 +160,33 @@ __global__ void __launch_bounds__(128) select_kernel(SelArgs a) {
     return;
   }
 
-  // candidate scores, ascending (frame, block)
+  const int budget = past_budget;
+  // candidate scores, ascending (frame, block).  Not needed when the global
+  // budget keeps every candidate and no scores are requested.  Four
+  // independent compensated dot products per lane hide the fp64 latency.
+  const bool need_scores = os != nullptr || a.per_frame || budget < C;
   const float* kb = a.k_block + (size_t)h * a.kb_head_stride;
-  for (int c = lane; c < C; c += 32) {
-    int t = fsel[c / bpf];
-    int blk = t * bpf + (c - (c / bpf) * bpf);
-    csc[c] = dot_f32_dd(kb + (size_t)blk * a.d, qv, a.d);
+  if (need_scores) {
+    for (int c0 = lane; c0 < C; c0 += 128) {
+      const float* rows[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + 32 * u;
+        ok[u] = c < C;
+        const int cc = ok[u] ? c : c0;
+        const int t = fsel[cc / bpf];
+        rows[u] = kb + (size_t)(t * bpf + (cc - (cc / bpf) * bpf)) * a.d;
+      }
+      double sc[4];
+      dot4_f32_dd(rows, qv, a.d, sc);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) csc[c0 + 32 * u] = sc[u];
+    }
   }
   __syncwarp();
 
-  const int budget = past_budget;
   const int per = (budget + nsel - 1) / nsel;
   const int take_pf = per < bpf ? per : bpf;
   int cnt = 0;

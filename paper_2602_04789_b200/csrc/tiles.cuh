@@ -50,6 +50,14 @@ __global__ void __launch_bounds__(128) plan_tiles_kernel(PlanArgs a) {
   int q1 = q0 + a.tile_rows;
   q1 = q1 < a.qt.total ? q1 : a.qt.total;
   const int qb0 = a.qt.block_of(q0), qb1 = a.qt.block_of(q1 - 1);
+  {  // nothing selected for this tile (e.g. a zero past budget): empty plan
+    int any = 0;
+    for (int j = lane; j <= qb1 - qb0 && j < 32; j += 32) any |= a.count[h * a.nqb + qb0 + j];
+    if (!__any_sync(0xffffffffu, any != 0)) {
+      if (lane == 0) a.seg_count[w] = 0;
+      return;
+    }
+  }
   for (int j = 0; j <= qb1 - qb0 && j < 32; ++j) {
     const int qb = qb0 + j;
     const int n = a.count[h * a.nqb + qb];
