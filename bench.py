@@ -636,9 +636,11 @@ def run_ours(args, c):
                          "traffic_source": traffic.get("attn_fwd", {}).get("source"),
                          "peak_source": tf_src,
                          "attn_ms_per_call": attn_ms, "flops_per_call": flops_call},
-            "roofline_select": {"bound": "hbm", "kernel": "pool_kernel (Q+K block pooling)",
+            "roofline_select": {"bound": "hbm", "kernel": "pool_frames_tma_kernel (Q+K block pooling)",
                                 "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                                 "frac": achieved_gbs / hbm_peak, "peak_source": hbm_src,
+                                "traffic": (traffic.get("pool", {}).get("bytes")
+                                            if args.config == "c2" else None),
                                 "bytes_per_call": pool_bytes,
                                 "pool_ms_per_call": pool_ms, "select_plan_ms_per_call": sel_ms},
             "cpu_baseline": cpu,
