@@ -15,6 +15,7 @@ from .errors import DegenerateScheduleError, EmptyActiveSetError, ZeroActiveRowE
 from .layout import AttnStats, BlockMask, ChunkLayout, ceil_div
 from .numerics import TopKResult, as_matrix, mean_pool, stable_softmax_row, topk_indices
 from .pipeline import HsaPipeline
+from .rollout import HsaRollout, largest_remainder_split, matched_budget_settings
 from .planner import (
     ChunkLengths,
     SparsityPlan,
@@ -53,4 +54,5 @@ __all__ = [
     "compress", "dense_attention", "frame_scores", "hsa_attention", "mean_pool", "plan_from_json",
     "plan_to_json", "round_half_up", "s_max_for_chunk", "select_blocks", "select_frames",
     "selection_trace", "solve_beta", "stable_softmax_row", "topk_indices", "tv_bound",
+    "HsaRollout", "largest_remainder_split", "matched_budget_settings",
 ]

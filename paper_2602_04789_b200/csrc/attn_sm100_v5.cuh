@@ -720,22 +720,35 @@ __global__ void __launch_bounds__(384, 1)
                                fmaxf(mx[6], mx[7]));
         uint64_t acc[2] = {0ull, 0ull};
         const uint64_t c2v = f2pack(c2, c2);
-        // P = 2^(s c2 - msub) for key chunks [c0, c1) (16 keys each) -> TMEM
+        // P = 2^(s c2 - msub) for key chunks [c0, c1) (16 keys each) -> TMEM.
+        // Three passes over the range (scale, exponentiate, sum + pack + store)
+        // so the 2x32 MUFU ops of a half issue back to back without waiting on
+        // their producers or consumers.
         auto exps = [&](int c0, int c1, float msub) {
           const uint64_t nm = f2pack(-msub, -msub);
+#pragma unroll
+          for (int ch = c0; ch < c1; ++ch)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              f2unpack(ffma2(f2pack(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]), c2v, nm),
+                       v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]);
+#pragma unroll
+          for (int ch = c0; ch < c1; ++ch)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              if (POLY > 0 && (8 * (ch & 1) + e) % POLY == POLY - 1) {
+                exp2_poly2(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]);
+              } else {
+                v[16 * ch + 2 * e] = ex2(v[16 * ch + 2 * e]);
+                v[16 * ch + 2 * e + 1] = ex2(v[16 * ch + 2 * e + 1]);
+              }
+            }
 #pragma unroll
           for (int ch = c0; ch < c1; ++ch) {
             uint32_t pk[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              float a, bb;
-              f2unpack(ffma2(f2pack(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]), c2v, nm), a, bb);
-              if (POLY > 0 && (8 * (ch & 1) + e) % POLY == POLY - 1) {
-                exp2_poly2(a, bb);
-              } else {
-                a = ex2(a);
-                bb = ex2(bb);
-              }
+              const float a = v[16 * ch + 2 * e], bb = v[16 * ch + 2 * e + 1];
               acc[e & 1] = fadd2(acc[e & 1], f2pack(a, bb));
               pk[e] = pack_bf16(a, bb);
             }
@@ -777,12 +790,10 @@ __global__ void __launch_bounds__(384, 1)
           // steady state: the first key half is exponentiated against the running
           // max while this tile's max is reduced alongside; only if some row max
           // grew by > 2^8 is that half redone after the rescale (rare)
-          exps(0, 4, m_used * c2);
           if (__any_sync(0xffffffffu, (fmaxf(m_used, mt) - m_used) * c2 > 8.0f)) {
-            update_max();
-            acc[0] = acc[1] = 0ull;
-            exps(0, 4, m_used * c2);
+            update_max();  // rare: a row max grew by > 2^8, rescale first
           }
+          exps(0, 4, m_used * c2);
         } else {
           update_max();
           exps(0, 4, m_used == -INFINITY ? 0.f : m_used * c2);

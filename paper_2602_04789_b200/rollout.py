@@ -169,3 +169,45 @@ class HsaRollout:
         return D.attention(q, self.kv_k[:, :lk], self.kv_v[:, :lk], qt, tiles, P * lay.n, lk,
                            out=out, out_dtype=self.out_dtype, scale=1.0 / math.sqrt(lay.d),
                            err=self.err, past_tiles=hint)
+
+
+# --------------------------------------------------------------------------- ablation settings
+# Host-side helpers of the reference's Fig. 2 ablation (rollout.py:333-374):
+# two budget settings matched in nominal FLOPs, run through FixedMaskBackend.
+
+def largest_remainder_split(total: int, weights) -> list:
+    """Split integer ``total`` in proportion to ``weights`` (largest remainder,
+    ties to the lowest index).  Restates rollout.py:333-347."""
+    import numpy as np
+    w = np.asarray(weights, dtype=np.float64)
+    if total < 0 or w.size == 0 or (w < 0).any() or w.sum() <= 0:
+        raise ValueError("need total >= 0 and positive weight mass")
+    exact = total * w / w.sum()
+    parts = np.floor(exact).astype(np.int64)
+    left = total - int(parts.sum())
+    rem = exact - parts
+    # stable order: larger remainder first, then lower index
+    order = sorted(range(w.size), key=lambda j: (-rem[j], j))
+    for j in order[:left]:
+        parts[j] += 1
+    return [int(x) for x in parts]
+
+
+def matched_budget_settings(layout, N: int, first_chunk_sparsity: float):
+    """Per-chunk row budgets (key blocks) of the two ablation settings, equal in
+    total: A sparsifies chunk 1 only, B keeps chunk 1 dense and removes the same
+    number of blocks from chunks 2..N in proportion to their context.
+    Restates rollout.py:350-374 (same errors)."""
+    from .planner import round_half_up
+    if not 0.0 < first_chunk_sparsity < 1.0:
+        raise ValueError(f"first_chunk_sparsity must lie in (0, 1), got {first_chunk_sparsity}")
+    if N < 2 or N > layout.N:
+        raise ValueError(f"need 2 <= N <= {layout.N}, got {N}")
+    full = [layout.k_blocks(i) for i in range(1, N + 1)]
+    keep = max(1, round_half_up((1.0 - first_chunk_sparsity) * full[0]))
+    a = [keep] + full[1:]
+    cut = largest_remainder_split(full[0] - keep, full[1:])
+    b = [full[0]] + [max(1, fb - c) for fb, c in zip(full[1:], cut)]
+    if sum(a) != sum(b):
+        raise ValueError("could not match totals; increase chunk sizes")
+    return a, b
