@@ -591,6 +591,14 @@ int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_hea
             frames_per_chunk, topk_frames, per_frame_mode ? 1 : 0, s_i_dev, cap, frame_cap,
             out_blocks, out_count, out_frames, out_scores, out_fscores, out_budget, wpc, spw,
             max_cand, (long long)kb_head_stride, (long long)kf_head_stride};
+  // one 4-warp CTA per (head, query block); its working set adds the flags
+  const int cta_smem = spw + (int)align_up((size_t)(P > max_cand ? P : max_cand), 16);
+  if (!getenv("LF_SELECT_WARP") && cta_smem <= 200 * 1024) {
+    if (cta_smem > 48 * 1024)
+      cudaFuncSetAttribute(select_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cta_smem);
+    select_cta_kernel<<<heads * nqb, 128, cta_smem, S(stream)>>>(a);
+    return check_launch("select_cta_kernel");
+  }
   const int smem = wpc * spw;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -234,3 +234,119 @@ __global__ void topk_kernel(const double* sc, int n, int k, int* out_idx) {
 }
 
 }  // namespace lf
+
+namespace lf {
+
+// K2 with one 128-thread CTA per (head, query block): the same selection as
+// select_kernel (same scores, same ranks, same ascending output) with the
+// frame scores, candidate scores and ranks spread over four warps, so four
+// times as many warps hide the fp64 latency chains (one warp per query block
+// left the SMs at ~10% warp occupancy).
+__global__ void __launch_bounds__(128) select_cta_kernel(SelArgs a) {
+  extern __shared__ __align__(16) unsigned char sel_smem[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int w = blockIdx.x;
+  const int h = w / a.nqb, r = w - h * a.nqb;
+  const int P = (a.chunk - 1) * a.f;
+  float* qv = reinterpret_cast<float*>(sel_smem);
+  double* fsc = reinterpret_cast<double*>(sel_smem + ((a.d * 4 + 15) & ~15));
+  int* fsel = reinterpret_cast<int*>(fsc + P);
+  double* csc = reinterpret_cast<double*>(fsel + ((a.frame_cap + 1) & ~1));
+  unsigned char* flag = reinterpret_cast<unsigned char*>(csc + a.max_cand);  // [max(P, C)]
+  __shared__ int s_nsel;
+
+  const float* qrow = a.q_block + ((size_t)h * a.nqb + r) * a.d;
+  for (int c = tid; c < a.d; c += 128) qv[c] = qrow[c];
+
+  const int current = a.f * a.bpf;
+  int total = current;
+  if (a.chunk > 1) total = (int)floor((1.0 - *a.s_i) * (double)(a.chunk * current) + 0.5);
+  const int past_budget = total > current ? total - current : 0;
+  if (a.out_budget && w == 0 && tid == 0) {
+    a.out_budget[0] = total;
+    a.out_budget[1] = past_budget;
+    a.out_budget[2] = total < current;
+  }
+  __syncthreads();
+
+  // frame scores and top-k flags
+  const float* kf = a.k_frame + (size_t)h * a.kf_head_stride;
+  for (int t = tid; t < P; t += 128) fsc[t] = dot_f32_dd(kf + (size_t)t * a.d, qv, a.d);
+  __syncthreads();
+  if (a.out_fscores) {
+    double* o = a.out_fscores + ((size_t)h * a.nqb + r) * P;
+    for (int t = tid; t < P; t += 128) o[t] = fsc[t];
+  }
+  const int kf_n = a.topk < P ? a.topk : P;
+  for (int t = tid; t < P; t += 128) flag[t] = kf_n > 0 && (kf_n >= P || stable_rank(fsc, 0, P, t) < kf_n);
+  __syncthreads();
+  if (tid < 32) {  // ascending compaction
+    int nsel = 0;
+    for (int b0 = 0; b0 < P; b0 += 32) {
+      const int t = b0 + lane;
+      const bool take = t < P && flag[t];
+      const unsigned m = __ballot_sync(0xffffffffu, take);
+      if (take) fsel[nsel + __popc(m & ((1u << lane) - 1))] = t;
+      nsel += __popc(m);
+    }
+    if (lane == 0) s_nsel = nsel;
+  }
+  __syncthreads();
+  const int nsel = s_nsel;
+  int* of = a.out_frames + ((size_t)h * a.nqb + r) * a.frame_cap;
+  for (int e = tid; e < a.frame_cap; e += 128) of[e] = e < nsel ? fsel[e] : -1;
+
+  const int bpf = a.bpf;
+  const int C = nsel * bpf;
+  if (C == 0 || past_budget == 0) {
+    if (tid == 0) a.out_count[w] = 0;
+    return;
+  }
+  int* ob = a.out_blocks + ((size_t)h * a.nqb + r) * a.cap;
+  double* os = a.out_scores ? a.out_scores + ((size_t)h * a.nqb + r) * a.cap : nullptr;
+  const int budget = past_budget;
+  const bool need_scores = os != nullptr || a.per_frame || budget < C;
+  const float* kb = a.k_block + (size_t)h * a.kb_head_stride;
+  if (need_scores) {
+    for (int c = tid; c < C; c += 128) {
+      const int t = fsel[c / bpf];
+      csc[c] = dot_f32_dd(kb + (size_t)(t * bpf + (c - (c / bpf) * bpf)) * a.d, qv, a.d);
+    }
+  }
+  __syncthreads();
+  const int per = (budget + nsel - 1) / nsel;
+  const int take_pf = per < bpf ? per : bpf;
+  for (int c = tid; c < C; c += 128) {
+    bool chosen;
+    if (!a.per_frame) {
+      chosen = budget >= C || stable_rank(csc, 0, C, c) < budget;
+    } else {
+      const int fi = c / bpf;
+      const int lr = stable_rank(csc, fi * bpf, bpf, c);
+      chosen = lr < per && fi * take_pf + lr < budget;
+    }
+    flag[c] = chosen;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int cnt = 0;
+    for (int b0 = 0; b0 < C; b0 += 32) {
+      const int c = b0 + lane;
+      const bool chosen = c < C && flag[c];
+      const unsigned m = __ballot_sync(0xffffffffu, chosen);
+      if (chosen) {
+        const int pos = cnt + __popc(m & ((1u << lane) - 1));
+        if (pos < a.cap) {
+          const int fi = c / bpf;
+          ob[pos] = fsel[fi] * bpf + (c - fi * bpf);
+          if (os) os[pos] = csc[c];
+        }
+      }
+      cnt += __popc(m);
+    }
+    if (lane == 0) a.out_count[w] = cnt < a.cap ? cnt : a.cap;
+  }
+}
+
+}  // namespace lf

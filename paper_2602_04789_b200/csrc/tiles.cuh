@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(128) plan_tiles_kernel(PlanArgs a) {
       unsigned int m = b < a.list_blocks ? qm[b] : 0u;
       const int c = ((m & maskA) ? 1 : 0) | ((m & maskB) ? 2 : 0);
       if (c != cls) m = 0u;
+      if (!__any_sync(0xffffffffu, m != 0u)) continue;  // nothing of this class here
       int s = 0, e = 0, pieces = 0;
       if (m) {
         s = a.kt.start(b);

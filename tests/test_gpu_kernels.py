@@ -52,6 +52,23 @@ def test_kernel_vs_oracle(lf, kernel, H, i, s_i, topk):
         assert_close_attn(out[h], ref, f"kernel {kernel} head {h}")
 
 
+@pytest.mark.parametrize("kernel", [TILE, PAIR])
+@pytest.mark.parametrize("n,f,i,d,s_i,topk", [(256, 2, 3, 64, 0.3, 2), (1536, 3, 5, 128, 0.6, 3),
+                                               (100, 1, 4, 64, 0.2, 2)])
+def test_kernel_small_shapes(lf, kernel, n, f, i, d, s_i, topk):
+    # config-1 shape (d = 64), the aligned 1536 layout, and a tiny ragged frame
+    H = 2
+    pipe, out, (q, k, v) = _run(lf, kernel, H, n, f, i, d, s_i, topk, seed=n + i)
+    out = out.cpu().numpy()
+    masks = pipe.masks()
+    for h in range(H):
+        _, sel = O.select(q[h], k[h], i, s_i, f, n, 64, 64, topk, "global", framewise=True)
+        np.testing.assert_array_equal(masks[h].bits, sel.bits)
+        ref, _ = O.block_sparse_attention(q[h], k[h], v[h], sel.bits, O.q_tiling(f, n, 64, True),
+                                          O.k_tiling(i, f, n, 64, True))
+        assert_close_attn(out[h], ref, f"kernel {kernel} n {n} head {h}")
+
+
 @pytest.mark.parametrize("H", [12, 2])
 def test_pair_bf16_epilogue_matches_fp32(lf, H):
     # bf16 output goes through the TMA-store epilogue (and, for H = 2, the
