@@ -657,6 +657,12 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
   wpc = wpc > 4 ? 4 : wpc;
   PlanArgs a{blocks, count, heads, nqb, cap, Tiling(q_tiling), Tiling(k_tiling), list_blocks,
              ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc, rows};
+  if (!getenv("LF_PLAN_WARP")) {
+    if (spw > 48 * 1024)
+      cudaFuncSetAttribute(plan_tiles_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, spw);
+    plan_tiles_cta_kernel<<<heads * ntiles, 128, spw, S(stream)>>>(a);
+    return check_launch("plan_tiles_cta_kernel");
+  }
   const int smem = wpc * spw;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(plan_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -96,3 +96,37 @@ def test_kernel_choice_is_reported(lf):
     assert lib.lf_attention_kernel_choice(12, 4680, 4680, 0) == TILE
     assert lib.lf_attention_kernel_choice(40, 4680, 4680, 0) == PAIR
     assert lib.lf_attention_kernel_choice(12, 4680, 4680, 226) == PAIR
+
+
+@pytest.mark.parametrize("i,s_i,topk", [(7, 0.5, 6), (14, 0.8, 6), (5, 0.0, 12)])
+def test_plan_kernels_agree(lf, i, s_i, topk):
+    # the 4-warp planner and the one-warp planner emit the same segment lists
+    # (pads may carry a different, always valid, start row)
+    import os
+    from paper_2602_04789_b200 import device as D
+    from paper_2602_04789_b200.selection import tilings
+    pipe, _, _ = _run(lf, TILE, 3, 1560, 3, i, 128, s_i, topk, seed=70 + i)
+    lay = lf.ChunkLayout(f=3, n=1560, b_q=64, b_kv=64, d=128, N=max(i, 7))
+    qt, kt = tilings(lay, i, True)
+    P = (i - 1) * 3
+    blocks, count, _, _ = pipe.selections()
+    plans = []
+    for env in (None, "1"):
+        if env:
+            os.environ["LF_PLAN_WARP"] = env
+        try:
+            t = D.plan_tiles(blocks, count, qt, kt, P * lay.frame_kv_blocks)
+            torch.cuda.synchronize()
+            plans.append((t.segs.cpu().numpy(), t.seg_count.cpu().numpy()))
+        finally:
+            os.environ.pop("LF_PLAN_WARP", None)
+    (s0, c0), (s1, c1) = plans
+    np.testing.assert_array_equal(c0, c1)
+    for idx in np.ndindex(c0.shape):
+        n = int(c0[idx])
+        a, b = s0[idx][:n].copy(), s1[idx][:n].copy()
+        pad = a[:, 1] == 0
+        np.testing.assert_array_equal(pad, b[:, 1] == 0)
+        a[pad, 0] = 0
+        b[pad, 0] = 0
+        np.testing.assert_array_equal(a, b)
