@@ -347,13 +347,32 @@ def run_ours(args, c):
     ro.kv_slot(i)[0].copy_(Kc[0])
     ro.kv_slot(i)[1].copy_(Vc[0])
 
+    # the selection half of step s+1 (pool q, select, plan; it reads only q and
+    # the committed summaries) runs on a side stream while step s attends
+    side = torch.cuda.Stream()
+    ev_prep = [torch.cuda.Event() for _ in range(T)]
+
     def chunk_flow():
+        main = torch.cuda.current_stream()
         if i > 1:
             ro.commit(None, None, i - 1, overwrite=True)
+        side.wait_stream(main)
+        plans = [None] * T
+
+        def prep(s):
+            with torch.cuda.stream(side):
+                plans[s] = ro.prepare(Q[s], i, s_i=s_dev, s_host=s_host)
+                ev_prep[s].record(side)
+        prep(0)
         for s in range(T):
-            ro.step(Q[s], None, None, i, s_i=s_dev, out=r_out[s], s_host=s_host)
+            if s + 1 < T:
+                prep(s + 1)
+            main.wait_event(ev_prep[s])
+            ro.attend(plans[s], out=r_out[s])
             if mode == "headshard":
                 gather_heads(r_out[s], shard, out=full[s])
+        main.wait_stream(side)
+        return plans
 
     flops_r = 0
     for s in range(T):
@@ -546,15 +565,26 @@ def run_ours(args, c):
                 ev_prev.record(s_h2d)
             cur.wait_event(ev_prev)
             ro.commit(None, None, i - 1, overwrite=True)
+        side.wait_stream(cur)
+        plans = [None] * T
+
+        def prep(s):
+            with torch.cuda.stream(side):
+                side.wait_event(ev_in[s & 1])
+                plans[s] = ro.prepare(stg_q[s & 1], i, s_i=s_dev, s_host=s_host)
+                ev_prep[s].record(side)
+        prep(0)
         for s in range(T):
             b = s & 1
             if s + 1 < T:
                 h2d(s + 1)
+                prep(s + 1)
             cur.wait_event(ev_in[b])
+            cur.wait_event(ev_prep[s])
             kc, vc = ro.kv_slot(i)
             kc.copy_(stg_k[b])
             vc.copy_(stg_v[b])
-            ro.step(stg_q[b], None, None, i, s_i=s_dev, out=r_out[s], s_host=s_host)
+            ro.attend(plans[s], out=r_out[s])
             ev_free[b].record(cur)
             if mode == "headshard":
                 gather_heads(r_out[s], shard, out=full[s])
@@ -563,6 +593,7 @@ def run_ours(args, c):
                 s_d2h.wait_event(ev_out[s])
                 hro[s].copy_(r_out[s], non_blocking=True)
         cur.wait_stream(s_d2h)  # the step ends when its outputs are on the host
+        cur.wait_stream(side)
 
     e2e_ms = timed(e2e_rollout, e2e_steps)
 
@@ -619,7 +650,7 @@ def run_ours(args, c):
                              f"{2 * h_local * lk * d * 2 / 1e6:.0f} MB)"},
             "e2e": {"value": flops_r_step / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                     "ms_per_chunk": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "HsaRollout.commit + HsaRollout.step (C ABI underneath); H2D / compute / D2H on three streams",
+                    "api": "HsaRollout.commit + prepare/attend (C ABI underneath); H2D, selection, attention and D2H on four streams",
                     "h2d_gbs_measured": h2d_gbs,
                     "pcie_bound_ms_per_chunk": h2d_only_ms},
             "stateless": {"value": value_stateless, "unit": UNIT, "ms_per_chunk": ms_step,
@@ -627,7 +658,7 @@ def run_ours(args, c):
                           "e2e_value": flops_step / (e2e_ms_sl * 1e-3) / 1e12,
                           "e2e_ms_per_chunk": e2e_ms_sl, "e2e_h2d_bytes_per_step": h2d_sl},
             "roofline": {"bound": "tensor",
-                         "kernel": ("attn_fwd_v5_kernel<128> (query-tile pairs)" if kernel_used == 5
+                         "kernel": ("attn_fwd_v5_kernel<128> (query-tile pairs)" if kernel_used >= 5
                                     else "attn_fwd_v3_kernel<128> (one query tile per CTA)"),
                          "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
                          "frac": achieved_tf / tf_peak,

@@ -141,16 +141,25 @@ class HsaRollout:
         q, k_cur, v_cur: bf16 [H, f*n, d] for the noisy current chunk.
         Past chunks 1..i-1 must have been committed.
         """
+        self.layout.check_chunk(int(chunk_index))
+        if k_cur is not None or v_cur is not None:
+            sl = self._slot(int(chunk_index))
+            if k_cur is not None:  # None: the caller already wrote them in place (kv_slot)
+                self.kv_k[:, sl].copy_(k_cur)
+            if v_cur is not None:
+                self.kv_v[:, sl].copy_(v_cur)
+        return self.attend(self.prepare(q, chunk_index, s_i=s_i, s_host=s_host), out=out)
+
+    def prepare(self, q: torch.Tensor, chunk_index: int, s_i=None, s_host=None) -> "StepPlan":
+        """Selection half of a step: pool q, hierarchical selection against the
+        cached summaries, tile plan.  Reads only q and the committed summaries
+        (not the current chunk's K/V), so a caller may run it for step s+1 on a
+        side stream while step s attends.  Enqueued on the current stream."""
         lay = self.layout
         i = int(chunk_index)
         lay.check_chunk(i)
         if self.committed != i - 1:
             raise ValueError(f"chunk {i} needs chunks 1..{i - 1} committed (have {self.committed})")
-        sl = self._slot(i)
-        if k_cur is not None:  # None: the caller already wrote them in place (kv_slot)
-            self.kv_k[:, sl].copy_(k_cur)
-        if v_cur is not None:
-            self.kv_v[:, sl].copy_(v_cur)
         qt, kt = tilings(lay, i, self.framewise)
         P = (i - 1) * lay.f
         q_block = D.pool_blocks(q, qt)
@@ -158,17 +167,38 @@ class HsaRollout:
         sel = D.select(q_block, self.kb_cache, self.kf_cache, self.bpf, i, lay.f,
                        self.cfg.topk_frames, self.cfg.block_budget_mode == "per-frame", s_dev)
         tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * self.bpf)
-        lk = lay.context_tokens(i)
-        self.last_selection = sel
-        self.last_chunk = i
         if s_host is None and s_i is not None and not torch.is_tensor(s_i):
             s_host = float(s_i)
         if s_host is None and s_i is None and self.plan is not None:
             s_host = float(self.plan.s[i - 1])
         hint = D.past_tiles_hint(s_host, i, lay.f, self.bpf, self.cfg.topk_frames, qt)
-        return D.attention(q, self.kv_k[:, :lk], self.kv_v[:, :lk], qt, tiles, P * lay.n, lk,
-                           out=out, out_dtype=self.out_dtype, scale=1.0 / math.sqrt(lay.d),
-                           err=self.err, past_tiles=hint)
+        self.last_selection = sel
+        self.last_chunk = i
+        return StepPlan(q, i, qt, q_block, sel, tiles, hint)
+
+    def attend(self, plan: "StepPlan", out: torch.Tensor | None = None) -> torch.Tensor:
+        """Attention half of a step: block-sparse attention of plan.q over the
+        cache (past chunks + the current chunk's K/V in its slot)."""
+        lay = self.layout
+        i = plan.chunk
+        P = (i - 1) * lay.f
+        lk = lay.context_tokens(i)
+        return D.attention(plan.q, self.kv_k[:, :lk], self.kv_v[:, :lk], plan.qt, plan.tiles,
+                           P * lay.n, lk, out=out, out_dtype=self.out_dtype,
+                           scale=1.0 / math.sqrt(lay.d), err=self.err, past_tiles=plan.hint)
+
+
+class StepPlan:
+    """Device results of HsaRollout.prepare (kept alive until attend has run)."""
+
+    def __init__(self, q, chunk, qt, q_block, selection, tiles, hint):
+        self.q = q
+        self.chunk = chunk
+        self.qt = qt
+        self.q_block = q_block
+        self.selection = selection
+        self.tiles = tiles
+        self.hint = hint
 
 
 # --------------------------------------------------------------------------- ablation settings
