@@ -2,7 +2,7 @@
 
 ``block_sparse_attention`` and ``dense_attention`` keep the reference's names,
 argument order, return values and exceptions; the work runs in the sm_100a
-tcgen05 kernel (csrc/attn_sm100.cuh) on bf16 copies of the operands with fp32
+tcgen05 kernels (csrc/attn_sm100_v3.cuh / _v5.cuh) on bf16 copies of the operands with fp32
 accumulation.  ``threads`` is accepted and ignored (the reference's
 ThreadPoolExecutor has no GPU analogue; results never depended on it).
 """

@@ -1,7 +1,7 @@
 // K4 v3: block-sparse flash attention, one persistent CTA per SM with a
 // double-buffered S/P in TMEM.
 //
-// Contract: attention.py:168-188, 229-274 restated (see attn_sm100.cuh).
+// Contract: attention.py:168-188, 229-274 restated (see attn_common.cuh).
 // Structure (10 warps):
 //   warp 0      TMA producer: Q of the work unit, K_j / V_j into 2-stage rings
 //   warp 1      TMEM owner + single-thread tcgen05.mma issuer
@@ -17,7 +17,7 @@
 // Work units are whole (head, query tile) items; the last partial round is
 // split over key tiles and merged by the last part to finish (as in v2).
 #pragma once
-#include "attn_sm100_v2.cuh"
+#include "attn_common.cuh"
 
 namespace lf {
 
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(64 + 128 * CG, 1)
           for (int e = 0; e < 16; ++e) {
             float a, bb;
             f2unpack(ffma2(f2pack(v[32 * ch + 2 * e], v[32 * ch + 2 * e + 1]), c2v, nm), a, bb);
-            if (POLY > 0 && e % POLY == POLY - 1) {
+            if (POLY > 0 && e % (POLY > 0 ? POLY : 1) == POLY - 1) {
               exp2_poly2(a, bb);  // FMA-pipe exponentials for 1/POLY of the pairs
             } else {
               a = ex2(a);

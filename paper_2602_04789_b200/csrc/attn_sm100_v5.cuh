@@ -1,6 +1,6 @@
 // K4 v5: block-sparse flash attention, two query tiles per CTA in ping-pong.
 //
-// Contract: attention.py:168-188, 229-274 restated (see attn_sm100.cuh): each
+// Contract: attention.py:168-188, 229-274 restated (see attn_common.cuh): each
 // query row takes the softmax over the keys of its active blocks only.
 //
 // A work item is a PAIR of 128-row query tiles (A = rows q0..q0+127,
@@ -29,7 +29,7 @@
 // equal contiguous ranges.  A split item writes unnormalised partials (O, m, l)
 // per part; the last part to finish merges them (split-KV identity).
 #pragma once
-#include "attn_sm100_v2.cuh"
+#include "attn_common.cuh"
 
 namespace lf {
 
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int ch = c0; ch < c1; ++ch)
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              if (POLY > 0 && (8 * (ch & 1) + e) % POLY == POLY - 1) {
+              if (POLY > 0 && (8 * (ch & 1) + e) % (POLY > 0 ? POLY : 1) == POLY - 1) {
                 exp2_poly2(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]);
               } else {
                 v[16 * ch + 2 * e] = ex2(v[16 * ch + 2 * e]);

@@ -6,10 +6,7 @@
 #include <cstring>
 #include <mutex>
 
-#include "attn_sm100.cuh"
-#include "attn_sm100_v2.cuh"
 #include "attn_sm100_v3.cuh"
-#include "attn_sm100_v4.cuh"
 #include "attn_sm100_v5.cuh"
 #include "cag.cuh"
 #include "pool.cuh"

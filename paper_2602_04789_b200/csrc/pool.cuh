@@ -286,7 +286,10 @@ template <int D>
 struct PoolTmaCfg {
   static constexpr int ROWS = 64;                    // block rows (b <= 64)
   static constexpr int STAGE = ROWS * D * 2;         // bytes
-  static constexpr int NST = 4;
+#ifndef LF_POOL_NST
+#define LF_POOL_NST 4
+#endif
+  static constexpr int NST = LF_POOL_NST;
   static constexpr int THREADS = 32 + D;             // producer warp + 2 groups x D/2 threads (2 cols each)
 };
 

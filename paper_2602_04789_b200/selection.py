@@ -4,7 +4,7 @@
 Names, argument order, return types and exceptions follow the reference.
 All arithmetic on the data runs on the GPU: pooling (csrc/pool.cuh), frame
 and block scoring + top-k (csrc/select.cuh), tile planning (csrc/tiles.cuh)
-and attention (csrc/attn_sm100.cuh).  Host code only validates arguments and
+and attention (csrc/attn_sm100_v3.cuh, csrc/attn_sm100_v5.cuh).  Host code only validates arguments and
 formats results (sorting a handful of selected indices, building the bool
 mask for callers that ask for it).
 
