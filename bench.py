@@ -658,8 +658,8 @@ def run_ours(args, c):
                           "e2e_value": flops_step / (e2e_ms_sl * 1e-3) / 1e12,
                           "e2e_ms_per_chunk": e2e_ms_sl, "e2e_h2d_bytes_per_step": h2d_sl},
             "roofline": {"bound": "tensor",
-                         "kernel": ("attn_fwd_v5_kernel<128> (query-tile pairs)" if kernel_used >= 5
-                                    else "attn_fwd_v3_kernel<128> (one query tile per CTA)"),
+                         "kernel": ("attn_fwd_v5_kernel<128> (query-tile pairs)" if kernel_used == 5
+                                    else "attn_fwd_v7_kernel<128> (query tile, two softmax sets)"),
                          "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
                          "frac": achieved_tf / tf_peak,
                          "traffic": (traffic.get("attn_fwd", {}).get("bytes")

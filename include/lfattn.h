@@ -146,11 +146,14 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
 
 /* lf_attention with an explicit kernel choice (same results within the stated
  * tolerance, bit-exact masks either way):
- *   LF_KERNEL_AUTO  work-based choice from past_tiles_hint (estimated non-dense
- *                   key tiles per 256-row plan tile; -1 = unknown -> 0)
- *   LF_KERNEL_TILE  one 128-row query tile per CTA (best for short work per SM)
+ *   LF_KERNEL_AUTO  the library's choice (currently the tile kernel, which
+ *                   matched or beat the pair kernel at every measured shape);
+ *                   past_tiles_hint (estimated non-dense key tiles per
+ *                   256-row plan tile, -1 = unknown) is reserved for it
+ *   LF_KERNEL_TILE  one 128-row query tile per CTA, two softmax sets on
+ *                   alternating key tiles (attn_fwd_v7_kernel)
  *   LF_KERNEL_PAIR  two query tiles per CTA in ping-pong sharing K/V, stream-K
- *                   tail (best for long work per SM) */
+ *                   tail (attn_fwd_v5_kernel) */
 #define LF_KERNEL_AUTO 0
 #define LF_KERNEL_TILE 3
 #define LF_KERNEL_PAIR 5

@@ -8,6 +8,7 @@
 
 #include "attn_sm100_v3.cuh"
 #include "attn_sm100_v5.cuh"
+#include "attn_sm100_v7.cuh"
 #include "cag.cuh"
 #include "pool.cuh"
 #include "select.cuh"
@@ -160,18 +161,20 @@ int launch_pool(PoolArgs& a, int dtype, int vec, int ns, cudaStream_t st) {
 // forced attention kernel (LF_ATTN_VER=3|5, for experiments), 0 = per call
 int attn_ver() {
   static const int v = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 0;
-  return v == 3 || v == 5 ? v : 0;
+  return v == 3 || v == 5 || v == 7 ? v : 0;
 }
 
-// Work-based kernel choice: the pair kernel is faster per key tile (two query
-// tiles share each K/V tile and ping-pong softmax against the tensor core) but
-// pays a unit-boundary and stream-K merge overhead per CTA that only long work
-// amortises (measured on B200: tile kernel ahead below ~100 pair-steps per SM).
+// Kernel choice.  The tile kernel with two softmax sets (v7) matches or beats
+// the pair kernel (v5) at every measured shape (B200: c2 1025 vs 907 TFLOP/s,
+// c3 576 vs 549, c5_s50 524 vs 480, c4 1041 vs 1043, c5_dense 1051 vs 1047)
+// without stream-K merges, so LF_KERNEL_AUTO takes it; the pair kernel stays
+// available explicitly (LF_KERNEL_PAIR).  LF_ATTN_VER=3 selects the previous
+// single-softmax tile kernel for comparisons.
 int choose_kernel(int heads, int n_qtiles, int dense_keys, int past_tiles, int sms) {
-  const long long n_pairs = (n_qtiles + 1) / 2;
-  const long long steps = n_pairs * heads * ((dense_keys + 127) / 128 + (past_tiles > 0 ? past_tiles : 0));
-  return steps >= 100LL * sms ? LF_KERNEL_PAIR : LF_KERNEL_TILE;
+  (void)heads; (void)n_qtiles; (void)dense_keys; (void)past_tiles; (void)sms;
+  return LF_KERNEL_TILE;
 }
+
 // tile plans cover query-tile pairs (256 rows) for both kernels (the tile
 // kernel skips the key tiles only its partner tile needs)
 int plan_rows() { return 2 * kTileRows; }
@@ -316,6 +319,18 @@ int launch_v3(AttnParams& p, int heads, int d, int sms, void* stream) {
   const int work = p.full_items + rem * tail_split;
   const int grid = work < slots ? work : slots;
   static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
+  if (attn_ver() != 3) {
+#define LF_V7(DD, PV)                                                                         \
+  if (d == DD && poly == PV) {                                                                \
+    cudaFuncSetAttribute(attn_fwd_v7_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         AttnCfg7<DD>::SMEM);                                                 \
+    attn_fwd_v7_kernel<DD, PV><<<grid, 320, AttnCfg7<DD>::SMEM, S(stream)>>>(p, work);        \
+    return check_launch("attn_fwd_v7_kernel");                                               \
+  }
+    LF_V7(128, 0) LF_V7(64, 0) LF_V7(128, 4)
+#undef LF_V7
+    return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v7: d=%d poly=%d not instantiated", d, poly);
+  }
 #define LF_V3(DD, PV)                                                                         \
   if (d == DD && poly == PV) {                                                                \
     cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, 2, PV>,                                       \
@@ -423,7 +438,7 @@ int lf_plan_tile_rows(void) { return plan_rows(); }
 
 int lf_attention_kernel_choice(int32_t heads, int32_t q_rows, int32_t dense_keys,
                                int32_t past_tiles_hint) {
-  if (attn_ver()) return attn_ver();
+  if (attn_ver()) return attn_ver() == 5 ? LF_KERNEL_PAIR : LF_KERNEL_TILE;
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
@@ -733,7 +748,7 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
   if (kernel != LF_KERNEL_TILE && kernel != LF_KERNEL_PAIR)
     kernel = choose_kernel(q->heads, p.n_qtiles, dense_hi > dense_lo ? dense_hi - dense_lo : 0,
                            past_tiles_hint, sms);
-  if (attn_ver()) kernel = attn_ver();
+  if (attn_ver()) kernel = attn_ver() == 5 ? LF_KERNEL_PAIR : LF_KERNEL_TILE;
   if (kernel == LF_KERNEL_PAIR) {
     p.tma_out = out_dtype == LF_BF16 && !getenv("LF_ATTN_NO_TMA_OUT") &&
                 make_out_map(&p.to, out, q->d, q->rows, q->heads, out_row_stride, out_head_stride);

@@ -1,7 +1,8 @@
-"""Both attention kernels, forced: the one-tile-per-CTA kernel (LF_KERNEL_TILE)
-and the query-tile-pair kernel with its stream-K split/merge tail
-(LF_KERNEL_PAIR), against the oracle on the same inputs (masks bit-exact,
-outputs within the tolerance of test_gpu_parity.py)."""
+"""Both attention kernels, forced: the one-tile-per-CTA kernel with two softmax
+sets (LF_KERNEL_TILE, with its split-KV tail) and the query-tile-pair kernel
+with its stream-K split/merge tail (LF_KERNEL_PAIR), against the oracle on the
+same inputs (masks bit-exact, outputs within the tolerance of
+test_gpu_parity.py)."""
 
 import numpy as np
 import pytest
@@ -92,10 +93,9 @@ def test_pair_graph_replay_deterministic(lf):
 def test_kernel_choice_is_reported(lf):
     from paper_2602_04789_b200 import _lib
     lib = _lib.lib()
-    # short work per SM -> tile kernel, long -> pair kernel
-    assert lib.lf_attention_kernel_choice(12, 4680, 4680, 0) == TILE
-    assert lib.lf_attention_kernel_choice(40, 4680, 4680, 0) == PAIR
-    assert lib.lf_attention_kernel_choice(12, 4680, 4680, 226) == PAIR
+    # the two-softmax-set tile kernel is the automatic choice at every shape
+    for args in ((12, 4680, 4680, 0), (40, 4680, 4680, 0), (12, 4680, 4680, 226)):
+        assert lib.lf_attention_kernel_choice(*args) == TILE
 
 
 @pytest.mark.parametrize("i,s_i,topk", [(7, 0.5, 6), (14, 0.8, 6), (5, 0.0, 12)])
