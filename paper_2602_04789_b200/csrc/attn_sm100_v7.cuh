@@ -31,8 +31,14 @@ struct AttnCfg7 {
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int SEG_BYTES = 64 * 128;
-  static constexpr int KST = 3;
-  static constexpr int VST = 2;
+#ifndef LF_V7_KST
+#define LF_V7_KST 2
+#endif
+#ifndef LF_V7_VST
+#define LF_V7_VST 3
+#endif
+  static constexpr int KST = LF_V7_KST;  // K ring stages
+  static constexpr int VST = LF_V7_VST;  // V ring stages
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
@@ -61,12 +67,13 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* p_full = bars + 4;    // [2 sets][2 key halves]
   uint64_t* o_full = bars + 8;
   uint64_t* o_empty = bars + 9;
-  uint64_t* k_full = bars + 10;   // [KST]
-  uint64_t* k_empty = bars + 13;  // [KST]
-  uint64_t* v_full = bars + 16;   // [VST]
-  uint64_t* v_empty = bars + 18;  // [VST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
-  int* flag = reinterpret_cast<int*>(bars + 21);
+  uint64_t* k_full = bars + 10;   // [KST <= 4]
+  uint64_t* k_empty = bars + 14;  // [KST]
+  uint64_t* v_full = bars + 18;   // [VST <= 4]
+  uint64_t* v_empty = bars + 22;  // [VST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+  int* flag = reinterpret_cast<int*>(bars + 27);
+  static_assert(C::KST <= 4 && C::VST <= 4, "barrier slots");
   float2* stat = reinterpret_cast<float2*>(smem + C::OFF_STAT);
 
   const int warp = threadIdx.x >> 5;
