@@ -229,7 +229,8 @@ def run_ours(args, c):
     import paper_2602_04789_b200 as lf
     from paper_2602_04789_b200 import device as D
     from paper_2602_04789_b200.selection import tilings
-    from paper_2602_04789_b200.sharding import gather_heads, partition_heads
+    from paper_2602_04789_b200.sharding import (gather_heads, gather_heads_overlapped,
+                                                partition_heads)
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -350,6 +351,7 @@ def run_ours(args, c):
     # the selection half of step s+1 (pool q, select, plan; it reads only q and
     # the committed summaries) runs on a side stream while step s attends
     side = torch.cuda.Stream()
+    comm = torch.cuda.Stream()
     ev_prep = [torch.cuda.Event() for _ in range(T)]
 
     def chunk_flow():
@@ -369,9 +371,11 @@ def run_ours(args, c):
                 prep(s + 1)
             main.wait_event(ev_prep[s])
             ro.attend(plans[s], out=r_out[s])
-            if mode == "headshard":
-                gather_heads(r_out[s], shard, out=full[s])
+            if mode == "headshard":  # all-gather of call s overlaps the compute of s+1
+                gather_heads_overlapped(r_out[s], shard, full[s], comm)
         main.wait_stream(side)
+        if mode == "headshard":
+            main.wait_stream(comm)
         return plans
 
     flops_r = 0
@@ -587,13 +591,15 @@ def run_ours(args, c):
             ro.attend(plans[s], out=r_out[s])
             ev_free[b].record(cur)
             if mode == "headshard":
-                gather_heads(r_out[s], shard, out=full[s])
+                gather_heads_overlapped(r_out[s], shard, full[s], comm)
             ev_out[s].record(cur)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev_out[s])
                 hro[s].copy_(r_out[s], non_blocking=True)
         cur.wait_stream(s_d2h)  # the step ends when its outputs are on the host
         cur.wait_stream(side)
+        if mode == "headshard":
+            cur.wait_stream(comm)
 
     e2e_ms = timed(e2e_rollout, e2e_steps)
 

@@ -53,3 +53,16 @@ def gather_heads(local: torch.Tensor, shard: HeadShard, out: torch.Tensor | None
         parts = list(out.split(shard.local_heads, dim=0))
         dist.all_gather(parts, local.contiguous(), group=group)
     return out
+
+
+def gather_heads_overlapped(local: torch.Tensor, shard: HeadShard, out: torch.Tensor,
+                            comm_stream: torch.cuda.Stream, group=None) -> None:
+    """gather_heads on ``comm_stream`` after the current stream's work so far:
+    the next call's compute overlaps this call's all-gather over NVLink (the
+    caller joins with ``current.wait_stream(comm_stream)`` before reading
+    ``out``)."""
+    if shard.mode != "headshard":
+        return
+    comm_stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(comm_stream):
+        gather_heads(local, shard, out=out, group=group)
