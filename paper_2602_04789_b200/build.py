@@ -30,19 +30,28 @@ def sources():
     return [os.path.join(d, f) for f in os.listdir(d)] + [hdr]
 
 
-def up_to_date() -> bool:
+STAMP = OUT + ".flags"  # the extra nvcc flags the library was built with
+
+
+def up_to_date(extra) -> bool:
     if not os.path.exists(OUT):
+        return False
+    try:
+        built_with = open(STAMP).read()
+    except OSError:
+        built_with = ""
+    if built_with != " ".join(extra):
         return False
     t = os.path.getmtime(OUT)
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+    extra = os.environ.get("LF_NVCC_FLAGS", "").split()  # e.g. -DLF_V7_TRACE (event trace builds)
+    if not force and up_to_date(extra):
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     tmp = OUT + ".tmp"
-    extra = os.environ.get("LF_NVCC_FLAGS", "").split()  # e.g. -DLF_V5_TRACE (event trace builds)
     cmd = [nvcc(), *FLAGS, *extra, "-o", tmp, SRC]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -52,6 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(tmp, OUT)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(extra))
     return OUT
 
 

@@ -51,6 +51,20 @@ struct AttnCfg7 {
   static constexpr int COL_O = 256;  // + 128 * set
 };
 
+// event trace (compile with -DLF_V7_TRACE, run with LF_ATTN_DEBUG=2, LF_ATTN_TRACE_CTA=c):
+// clock64 stamps of CTA c -- softmax [X][k][8] at X*512 (wait start, S ready, stats done,
+// P half 0, P half 1); MMA [kit][4] at 1024 (QK issued, PV wait start, PV issued, K wait
+// start) and K ready at 3072 + kit; items [n][8] at 1536 (producer Q issued, MMA item
+// start, set 0 tail start / O ready / done, set 1 the same).  scripts/trace_v7.py prints it.
+#ifdef LF_V7_TRACE
+#define LF_T7(idx, val) \
+  if ((p.debug & 255) == 2 && (int)blockIdx.x == (p.debug >> 8) && p.trace) p.trace[idx] = (val)
+#else
+#define LF_T7(idx, val) \
+  do {                  \
+  } while (0)
+#endif
+
 template <int D, int POLY>
 __global__ void __launch_bounds__(320, 1)
     attn_fwd_v7_kernel(const __grid_constant__ AttnParams p, int total_work) {
@@ -117,6 +131,7 @@ __global__ void __launch_bounds__(320, 1)
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
+      if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8, clk64());
       mbar_wait(q_empty, (nq++ & 1) ^ 1);
       if (elect_one()) {
         mbar_expect_tx(q_full, C::Q_BYTES);
@@ -124,8 +139,13 @@ __global__ void __launch_bounds__(320, 1)
           tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, wi.tile * C::BM, wi.h);
       }
       __syncwarp();
+      TileSegs nx0, nx1;  // the next two entries, loaded ahead (their latency off the loop)
+      if (cx.j0 < cx.j1) nx0 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0);
+      if (cx.j0 + 1 < cx.j1) nx1 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0 + 1);
       for (int j = cx.j0; j < cx.j1; ++j) {
-        const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
+        const TileSegs ts = nx0;
+        nx0 = nx1;
+        if (j + 2 < cx.j1) nx1 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j + 2);
         if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;
         const int ks = kit % C::KST, vs = kit % C::VST;
         mbar_wait(k_empty + ks, ((kit / C::KST) & 1) ^ 1);
@@ -163,7 +183,9 @@ __global__ void __launch_bounds__(320, 1)
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
-      mbar_wait(q_full, nq++ & 1);
+      mbar_wait(q_full, nq & 1);
+      if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8 + 1, clk64());
+      ++nq;
       int pend[2] = {-1, -1};
       uint32_t pend_kit[2] = {0, 0};
       bool first_pv[2] = {true, true}, waited_o = false;
@@ -171,6 +193,7 @@ __global__ void __launch_bounds__(320, 1)
       auto issue_pv = [&](int x) {
         const uint32_t t = pend_kit[x];
         const int vs = t % C::VST;
+        if (lane == 0 && t < 120) LF_T7(1024 + t * 4 + 1, clk64());
         if (!waited_o) {  // O_0 / O_1 are free once the previous epilogue read them
           mbar_wait(o_empty, (noe & 1) ^ 1);
           ++noe;
@@ -191,17 +214,25 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
         ++np[x];
+        if (lane == 0 && t < 120) LF_T7(1024 + t * 4 + 2, clk64());
         tc_commit_elect(v_empty + vs);
         first_pv[x] = false;
         pend[x] = -1;
       };
+      TileSegs nx0, nx1;  // the next two entries, loaded ahead (their latency off the loop)
+      if (cx.j0 < cx.j1) nx0 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0);
+      if (cx.j0 + 1 < cx.j1) nx1 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0 + 1);
       for (int j = cx.j0; j < cx.j1; ++j) {
-        const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
+        const TileSegs ts = nx0;
+        nx0 = nx1;
+        if (j + 2 < cx.j1) nx1 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j + 2);
         if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;
         const int x = k & 1;
         const int ks = kit % C::KST;
         if (pend[x] >= 0) issue_pv(x);  // P_x of its previous tile still sits in S_x
+        if (lane == 0 && kit < 120) LF_T7(1024 + kit * 4 + 3, clk64());
         mbar_wait(k_full + ks, (kit / C::KST) & 1);
+        if (lane == 0 && kit < 120) LF_T7(3072 + kit, clk64());
         tc_fence_after();
         const uint64_t kd = kd0 + ((uint32_t)(ks * C::KV_BYTES) >> 4);
 #pragma unroll
@@ -212,6 +243,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         tc_commit_elect(s_full + x);
         tc_commit_elect(k_empty + ks);
+        if (lane == 0 && kit < 120) LF_T7(1024 + kit * 4, clk64());
         pend[x] = 1;
         pend_kit[x] = kit;
         ++kit;
@@ -239,8 +271,9 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t s_col = C::COL_S + X * 128;
     const uint32_t o_col = C::COL_O + X * 128;
     const float c2 = p.scale_log2;
-    uint32_t ns = 0, no = 0;
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+    uint32_t ns = 0, no = 0, nitem = 0;
+    const bool tr = (warp == 2 || warp == 6) && lane == 0;  // one thread per set
+    for (int w = blockIdx.x; w < total_work; w += gridDim.x, ++nitem) {
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       const int grow = wi.tile * 128 + row;
@@ -259,7 +292,9 @@ __global__ void __launch_bounds__(320, 1)
         const bool row_full =
             !row_ok || (((ts.m0 & ts.m1) >> lq & 1) && ts.l0 == 64 && ts.l1 == 64);
         const bool full = __all_sync(0xffffffffu, row_full);
+        if (tr && ns < 60) LF_T7(X * 512 + ns * 8, clk64());
         mbar_wait(s_full + X, ns & 1);
+        if (tr && ns < 60) LF_T7(X * 512 + ns * 8 + 1, clk64());
         ++ns;
         tc_fence_after();
         float v[128];
@@ -301,6 +336,7 @@ __global__ void __launch_bounds__(320, 1)
             tmem_st16(t_row + o_col + c * 16, reinterpret_cast<uint32_t*>(o));
           }
         }
+        if (tr && ns - 1 < 60) LF_T7(X * 512 + (ns - 1) * 8 + 2, clk64());
         const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
         const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
 #pragma unroll
@@ -334,6 +370,7 @@ __global__ void __launch_bounds__(320, 1)
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(p_full + 2 * X + hh);
+          if (tr && ns - 1 < 60) LF_T7(X * 512 + (ns - 1) * 8 + 3 + hh, clk64());
         }
         acc[0] = fadd2(acc[0], acc[1]);
         float a, bb;
@@ -347,11 +384,13 @@ __global__ void __launch_bounds__(320, 1)
       }
       // ---- merge the two sets' states (split-KV identity) and write out
       stat[X * 128 + row] = make_float2(m_used, kx > 0 ? l : 0.f);
+      if (tr && nitem < 16) LF_T7(1536 + nitem * 8 + 2 + X * 3, clk64());
       if (k > 0) {
         mbar_wait(o_full, no & 1);
         ++no;
         tc_fence_after();
       }
+      if (tr && nitem < 16) LF_T7(1536 + nitem * 8 + 3 + X * 3, clk64());
       asm volatile("bar.sync 1, 256;" ::: "memory");
       const float2 s0 = stat[row], s1 = stat[128 + row];
       const float M = fmaxf(s0.y > 0.f ? s0.x : -INFINITY, s1.y > 0.f ? s1.x : -INFINITY);
@@ -387,6 +426,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         tc_fence_before();
         mbar_arrive(o_empty);  // O_0 / O_1 read: the next item's first PV may overwrite them
+        if (tr && nitem < 16) LF_T7(1536 + nitem * 8 + 4 + X * 3, clk64());
       }
       if (wi.nparts == 1) {
         if (row_ok && k > 0 && X == 0 && p.lse)

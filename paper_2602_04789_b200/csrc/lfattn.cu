@@ -235,6 +235,33 @@ bool split_scratch(size_t need_c, size_t need_ml, size_t need_o, cudaStream_t st
 }
 
 // v5: query-tile pairs; whole items round-robin, the tail (< grid items) stream-K
+// benchmarking probes: LF_ATTN_DEBUG=1 skips the softmax arithmetic; =2 records the
+// clock64 event trace of CTA LF_ATTN_TRACE_CTA (kernels built with the trace macro)
+// and writes it to gpurun_out/attn_trace.txt after the fourth launch
+void setup_trace(AttnParams& p, void* stream) {
+  p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
+  if (p.debug == 2 && getenv("LF_ATTN_TRACE_CTA")) p.debug |= atoi(getenv("LF_ATTN_TRACE_CTA")) << 8;
+  if ((p.debug & 255) == 2) {
+    static long long* tr = nullptr;
+    if (!tr) {
+      cudaMalloc(&tr, 4096 * 8);
+      cudaMemset(tr, 0, 4096 * 8);
+    }
+    p.trace = tr;
+    static int dumps = 0;
+    if (dumps++ == 3) {  // dump after a few launches (ordered with the stream)
+      cudaStreamSynchronize(S(stream));
+      static long long h[4096];
+      cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
+      FILE* f = fopen("gpurun_out/attn_trace.txt", "w");
+      if (f) {
+        for (int i = 0; i < 4096; ++i) fprintf(f, "%lld\n", h[i]);
+        fclose(f);
+      }
+    }
+  }
+}
+
 int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
   const int n_pairs = (p.n_qtiles + 1) / 2;
   const int items = n_pairs * heads;
@@ -257,29 +284,9 @@ int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
   }
   const int grid = items < G && !p.part_o ? items : G;
   if (grid <= 0) return LF_OK;
-  p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
-  if (p.debug == 2 && getenv("LF_ATTN_TRACE_CTA")) p.debug |= atoi(getenv("LF_ATTN_TRACE_CTA")) << 8;
-  if ((p.debug & 255) == 2) {
-    static long long* tr = nullptr;
-    if (!tr) {
-      cudaMalloc(&tr, 4096 * 8);
-      cudaMemset(tr, 0, 4096 * 8);
-    }
-    p.trace = tr;
-    static int dumps = 0;
-    if (dumps++ == 3) {  // dump after a few launches (ordered with the stream)
-      cudaStreamSynchronize(S(stream));
-      static long long h[4096];
-      cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
-      FILE* f = fopen("gpurun_out/attn_trace.txt", "w");
-      if (f) {
-        for (int i = 0; i < 4096; ++i) fprintf(f, "%lld\n", h[i]);
-        fclose(f);
-      }
-    }
-  }
+  setup_trace(p, stream);
   static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
-#define LF_V5(DD, PV)                                                                         \
+#define LF_V5(DD, PV)                                                                            \
   if (d == DD && poly == PV) {                                                                \
     cudaFuncSetAttribute(attn_fwd_v5_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          AttnCfg5<DD>::SMEM);                                                 \
@@ -315,7 +322,7 @@ int launch_v3(AttnParams& p, int heads, int d, int sms, void* stream) {
   }
   p.full_items = items - rem;
   p.tail_split = tail_split;
-  p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
+  setup_trace(p, stream);
   const int work = p.full_items + rem * tail_split;
   const int grid = work < slots ? work : slots;
   static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;

@@ -10,5 +10,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 2 -c 1 -o gpurun_out/attn_c2 python bench.py --profile-launch --no-cpu-baseline > gpurun_out/ncu_attn.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 2 -c 1 -o gpurun_out/attn_c5_dense python bench.py --profile-launch --no-cpu-baseline --config c5_dense > gpurun_out/ncu_attn5.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:pool_frames -s 2 -c 1 -o gpurun_out/pool_c2 python bench.py --profile-launch --no-cpu-baseline > gpurun_out/ncu_pool.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:select_kernel -s 2 -c 1 -o gpurun_out/select_c5_dense python bench.py --profile-launch --no-cpu-baseline --config c5_dense > gpurun_out/ncu_select.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:select_cta -s 2 -c 1 -o gpurun_out/select_c5_dense python bench.py --profile-launch --no-cpu-baseline --config c5_dense > gpurun_out/ncu_select.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:select_cta -s 2 -c 1 -o gpurun_out/select_c3 python bench.py --profile-launch --no-cpu-baseline --config c3 > gpurun_out/ncu_select3.log 2>&1
 tail -n 3 gpurun_out/*.err
