@@ -39,7 +39,23 @@ struct SelArgs {
 
 __device__ __forceinline__ double dot_f32_dd(const float* __restrict__ row, const float* qv, int d) {
   DD acc{0.0, 0.0};
-  if ((d & 3) == 0 && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+  if ((d & 31) == 0 && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+    // 32 elements per batch: the 8 loads go out together, then the sequential
+    // compensated sum (same order as element by element)
+    for (int c0 = 0; c0 < d; c0 += 32) {
+      float4 x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(row + c0) + u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + 4 * u;
+        dd_add(acc, (double)x[u].x * (double)qv[c]);
+        dd_add(acc, (double)x[u].y * (double)qv[c + 1]);
+        dd_add(acc, (double)x[u].z * (double)qv[c + 2]);
+        dd_add(acc, (double)x[u].w * (double)qv[c + 3]);
+      }
+    }
+  } else if ((d & 3) == 0 && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
     for (int c = 0; c < d; c += 4) {
       float4 a = __ldg(reinterpret_cast<const float4*>(row + c));
       dd_add(acc, (double)a.x * (double)qv[c]);
