@@ -227,21 +227,24 @@ def issued_mma_flops(plan, d):
     4*128*128*d (QK^T + PV), whatever part of it the selection needs (rows of
     a tile share the union of their query blocks' key blocks)."""
     import numpy as np
+    from paper_2602_04789_b200 import device as dv
     qt = plan.qt
     H = plan.q.shape[0]
+    mode = getattr(plan, "qmode", None)
+    mode = dv.qtile_mode(qt) if mode is None else mode
+    nq = -(-qt.count // 2) if mode else -(-qt.total // 128)
     tq = -(-qt.total // 128)
-    dense = tq * tq * H  # the current chunk: every query tile x every chunk key tile
+    dense = nq * tq * H  # the current chunk: every query tile x every chunk key tile
     if plan.tiles is None:  # chunk 1: no past
         return dense * 4 * 128 * 128 * d
     segs = plan.tiles.segs.cpu().numpy()
     cnt = plan.tiles.seg_count.cpu().numpy()
     ntiles = cnt.shape[1]
-    rows = 256
     total = 0
     for t in range(ntiles):
-        q0, q1 = t * rows, min(t * rows + rows, qt.total)
+        q0, mid = dv.qtile_rows(qt, mode, 2 * t)
+        q1 = dv.qtile_rows(qt, mode, 2 * t + 1)[1] if 2 * t + 1 < nq else mid
         qb0 = qt.block_of(q0)
-        mid = min(q0 + 128, q1)
 
         def bits(r0, r1):
             if r0 >= r1:
@@ -459,6 +462,7 @@ def run_ours(args, c):
     bpf = lay.frame_kv_blocks
     P = (i - 1) * f
     hint = D.past_tiles_hint(s_host, i, f, bpf, c["topk"], qt)
+    qmode = D.auto_qtile_mode(s_host, i, f, bpf, c["topk"])  # as HsaRollout.prepare picks it
     from paper_2602_04789_b200 import _lib as LL
     kernel_used = int(LL.lib().lf_attention_kernel_choice(h_local, lq, lq, hint))
     stage = {"pool": [], "select": [], "attn": []}
@@ -472,11 +476,13 @@ def run_ours(args, c):
         def run_sel(s=s, st=st):
             qb, kb, kf = st["views"]
             sel = D.select(qb, kb, kf, bpf, i, f, c["topk"], c["mode"] == "per-frame", s_dev)
-            st["tiles"] = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf)
+            with D.qtile_scope(qmode):
+                st["tiles"] = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf)
 
         def run_attn(s=s, st=st):
-            D.attention(Q[s], K[s], V[s], qt, st["tiles"], P * n, lk, out=outs[s],
-                        past_tiles=hint)
+            with D.qtile_scope(qmode):
+                D.attention(Q[s], K[s], V[s], qt, st["tiles"], P * n, lk, out=outs[s],
+                            past_tiles=hint)
 
         fns = (run_pool, run_sel, run_attn)
         for fn in fns:  # warm (allocates the static buffers the graphs reuse)
@@ -694,6 +700,9 @@ def run_ours(args, c):
                        "heads": H, "d": d, "n": n, "f": f, "chunk": i, "N": c["N"],
                        "plan": list(c["plan"]) if c["plan"] else None, "s_i": s_host,
                        "topk_frames": c["topk"], "mode": c["mode"], "parallelism": mode,
+                       "query_tiles": ("block-aligned (2 query blocks)" if (
+                           os.environ.get("LF_QTILE", "") == "blocks" or (
+                               not os.environ.get("LF_QTILE") and qmode)) else "128-row"),
                        "l2": "inputs larger than L2 (K+V per call "
                              f"{2 * h_local * lk * d * 2 / 1e6:.0f} MB)"},
             "e2e": {"value": flops_r_step / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,

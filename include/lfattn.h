@@ -119,6 +119,24 @@ int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f,
  * tiles; both attention kernels read these plans). */
 int lf_plan_tile_rows(void);
 
+/* Query-tile geometry (an extension, no reference counterpart: it only changes
+ * how rows are grouped into tensor-core tiles, never the result).
+ * lf_set_qtile_mode(1) asks for block-aligned query tiles -- two consecutive
+ * query blocks per tile, so a ragged framewise tiling (n = 1560, b = 64) never
+ * puts 3 query blocks' selections into one tile; plan tile t then covers query
+ * tiles 2t and 2t+1 (four query blocks).  0 = 128-row tiles at multiples of
+ * 128.  -1 (default): the LF_QTILE environment variable ("blocks" / "rows")
+ * when set, else 128-row tiles for lf_plan_tiles / lf_attention(_ex), and an
+ * automatic choice inside each lf_hsa_* call (block-aligned when s_i_host
+ * gives >= 16 past blocks per query block).  Applies
+ * to tilings with 33..64-row blocks; lf_qtile_mode() returns the mode a tiling
+ * gets, lf_plan_tile_count() its number of plan tiles (the `ntiles` of the
+ * lf_plan_tiles outputs).  Set it before planning; the planner and the
+ * attention call of one step must see the same mode. */
+void lf_set_qtile_mode(int32_t mode);
+int lf_qtile_mode(lf_tiling q_tiling);
+int lf_plan_tile_count(lf_tiling q_tiling);
+
 /* Per plan tile (lf_plan_tile_rows() rows): union of its query blocks' active
  * key blocks as <=64-key segments {token start, length, query-block bitmask, 0}.
  * Segments from block lists `blocks[H][nqb][cap]` / `count[H][nqb]` over the

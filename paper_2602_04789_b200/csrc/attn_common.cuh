@@ -42,6 +42,7 @@ struct AttnParams {
   CUtensorMap to;    // v5: bf16 output map (box 64 cols x 32 rows), valid when tma_out
   int tma_out;
   int plan_pairs;    // segs are 256-row (pair) plans
+  int qmode;         // query-tile geometry (qtile_rows in common.cuh); 1 implies plan_pairs
   float* part_o;    // split partials (tile kernel: fp32 [part][128][D]; pair kernel: fp16 O/l)
   float2* part_ml;  // [part][rows] (row max, row sum)
   int* counters;    // [tail], zero between launches
@@ -125,11 +126,10 @@ struct TileCtx {
   const int4* segs;
   uint32_t qm;      // query-block bits of this 128-row tile in its plan (all: 128-row plans)
   int q0;           // first row of the plan tile (qmask bits are relative to its block)
+  int x0, x1;       // this query tile's rows [x0, x1)
 };
-__device__ __forceinline__ uint32_t tile_qmask(const AttnParams& p, int q0, int x0) {
-  if (x0 >= p.Lq) return 0u;
-  int x1 = x0 + 128;
-  x1 = x1 < p.Lq ? x1 : p.Lq;
+__device__ __forceinline__ uint32_t tile_qmask(const AttnParams& p, int q0, int x0, int x1) {
+  if (x0 >= x1) return 0u;
   const int b0 = p.qt.block_of(q0);
   int lo = p.qt.block_of(x0) - b0, hi = p.qt.block_of(x1 - 1) - b0;
   hi = hi < 31 ? hi : 31;
@@ -142,8 +142,14 @@ __device__ __forceinline__ TileCtx tile_ctx(const AttnParams& p, WorkItem wi) {
   TileCtx c;
   const int n_pairs = (p.n_qtiles + 1) >> 1;
   const int wid = p.plan_pairs ? wi.h * n_pairs + (wi.tile >> 1) : wi.h * p.n_qtiles + wi.tile;
-  c.q0 = p.plan_pairs ? (wi.tile >> 1) * 256 : wi.tile * 128;
-  c.qm = p.plan_pairs ? tile_qmask(p, c.q0, wi.tile * 128) : 0xffffffffu;
+  qtile_rows(p.qt, p.qmode, wi.tile, c.x0, c.x1);
+  if (p.qmode) {
+    int e;
+    qtile_rows(p.qt, 1, wi.tile & ~1, c.q0, e);
+  } else {
+    c.q0 = p.plan_pairs ? (wi.tile >> 1) * 256 : wi.tile * 128;
+  }
+  c.qm = p.plan_pairs ? tile_qmask(p, c.q0, c.x0, c.x1) : 0xffffffffu;
   c.nseg = p.seg_count ? p.seg_count[wid] : 0;
   c.segs = p.segs ? p.segs + (size_t)wid * p.seg_cap : nullptr;
   c.Tp = (c.nseg + 1) >> 1;

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(320, 1)
       if (elect_one()) {
         mbar_expect_tx(q_full, C::Q_BYTES);
         for (int a = 0; a < C::ATOMS; ++a)
-          tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, wi.tile * C::BM, wi.h);
+          tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, cx.x0, wi.h);
       }
       __syncwarp();
       TileSegs nx0, nx1;  // the next two entries, loaded ahead (their latency off the loop)
@@ -276,8 +276,8 @@ __global__ void __launch_bounds__(320, 1)
     for (int w = blockIdx.x; w < total_work; w += gridDim.x, ++nitem) {
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
-      const int grow = wi.tile * 128 + row;
-      const bool row_ok = grow < p.Lq;
+      const int grow = cx.x0 + row;
+      const bool row_ok = grow < cx.x1;
       int lq = 0;
       if (row_ok) {
         lq = p.qt.block_of(grow) - p.qt.block_of(cx.q0);

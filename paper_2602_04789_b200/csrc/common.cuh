@@ -41,6 +41,27 @@ struct Tiling {
   }
 };
 
+// Query-tile geometry shared by the tile planner and the attention kernels.
+// Mode 0: 128-row query tiles at multiples of 128 (a tile may straddle 3 query
+// blocks of a ragged framewise tiling). Mode 1 (block-aligned): a query tile is
+// two consecutive query blocks (<= 128 rows when block <= 64), so its key-block
+// union covers 2 blocks' selections, never 3. Plan tiles pair query tiles
+// (2t, 2t+1) in both modes.
+__host__ __device__ inline int qtile_count(const Tiling& qt, int mode) {
+  return mode ? (qt.count() + 1) / 2 : (qt.total + 127) / 128;
+}
+// rows [x0, x1) of query tile t
+__host__ __device__ inline void qtile_rows(const Tiling& qt, int mode, int t, int& x0, int& x1) {
+  if (mode) {
+    const int nb = qt.count();
+    x0 = qt.start(2 * t);
+    x1 = 2 * t + 2 < nb ? qt.start(2 * t + 2) : qt.total;
+  } else {
+    x0 = t * 128;
+    x1 = x0 + 128 < qt.total ? x0 + 128 : qt.total;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // compensated fp64 accumulation (TwoSum), used for the selection dot products
 // so that equal inputs give equal scores and near-ties are resolved by the

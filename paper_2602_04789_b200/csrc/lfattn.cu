@@ -11,6 +11,9 @@
 #include "attn_sm100_v7.cuh"
 #include "cag.cuh"
 #include "pool.cuh"
+#ifndef LF_POOL_DEFAULT
+#define LF_POOL_DEFAULT 1
+#endif
 #include "select.cuh"
 #include "tiles.cuh"
 
@@ -189,6 +192,52 @@ int max_qblocks_per_tile(lf_tiling qt, int rows = kTileRows) {
   }
   return worst;
 }
+
+// Query-tile geometry (qtile_rows in common.cuh) for a query tiling: 1 =
+// block-aligned tiles (two query blocks each) when requested (lf_set_qtile_mode,
+// else LF_QTILE=blocks) and the blocks are 33..64 rows, else 0 = 128-row tiles.
+// The tile planner and the attention kernel must agree: both read it here.
+int g_qmode_req = -1;                 // lf_set_qtile_mode
+thread_local int g_qmode_scope = -1;  // automatic choice of the lf_hsa_* call in progress
+constexpr int kBlockTilesMinPast = 16;
+int qmode_for(lf_tiling qt) {
+  int req = g_qmode_req;
+  if (req < 0) {
+    const char* e = getenv("LF_QTILE");
+    if (e && *e) req = !strcmp(e, "blocks") ? 1 : 0;
+  }
+  if (req < 0) req = g_qmode_scope > 0 ? 1 : 0;
+  return req && qt.block > 32 && qt.block <= 64 ? 1 : 0;
+}
+// Automatic geometry for one selection step, from the host copy of s_i: the
+// estimated past blocks per query block (budget (1-s_i)*i*f*bpf minus the
+// current chunk, capped at topk*bpf). Block-aligned tiles pay when it is >= 16
+// and below all past blocks (measured: +12 % at chunk 14 / 25 past blocks,
+// +10-17 % at 83-150; -2 % at 4, -19 % at 0 and -7 % when every past block is
+// selected, where the extra partial tiles only add work and a tail round).
+int auto_qmode(double s, int chunk, int f, int n, int b_kv, int topk) {
+  const int P = (chunk - 1) * f;
+  if (!(s >= 0.0 && s < 1.0) || P <= 0 || b_kv < 1) return 0;
+  const int bpf = (n + b_kv - 1) / b_kv, cur = f * bpf;
+  long long past = (long long)((1.0 - s) * chunk * cur + 0.5) - cur;
+  const long long cap = (long long)(topk < P ? topk : P) * bpf;
+  past = past < cap ? past : cap;
+  // every past block selected: all query blocks share one list, nothing to gain
+  return past >= kBlockTilesMinPast && past < (long long)P * bpf ? 1 : 0;
+}
+struct QmodeScope {
+  int prev;
+  explicit QmodeScope(int m) : prev(g_qmode_scope) { g_qmode_scope = m; }
+  ~QmodeScope() { g_qmode_scope = prev; }
+};
+QmodeScope hsa_qmode_scope(const lf_hsa_args* a) {
+  return QmodeScope(auto_qmode(a->s_i_host, a->chunk_index, a->f, a->n, a->b_kv, a->topk_frames));
+}
+int plan_tile_count(lf_tiling qt) {
+  if (qmode_for(qt)) return (qtile_count(Tiling(qt), 1) + 1) / 2;
+  return (qt.total + plan_rows() - 1) / plan_rows();
+}
+int max_qblocks(lf_tiling qt) { return qmode_for(qt) ? 4 : max_qblocks_per_tile(qt, plan_rows()); }
 
 // segment capacity of one tile plan: <= mq query blocks x cap selected blocks,
 // <= all past blocks, each cut in ceil(b_kv/64) pieces, + 3 class pads
@@ -377,12 +426,11 @@ int hsa_geom(const lf_hsa_args* a, HsaGeom* g) {
   int kf = a->topk_frames < g->P ? a->topk_frames : g->P;
   g->frame_cap = kf > 0 ? kf : 1;
   g->cap = kf * g->bpf > 0 ? kf * g->bpf : 1;
-  const int rows = plan_rows();
-  g->ntiles = (Lq + rows - 1) / rows;
+  g->ntiles = plan_tile_count(g->qt);
   g->list_blocks = g->P * g->bpf;
-  int mq = max_qblocks_per_tile(g->qt, rows);
+  int mq = max_qblocks(g->qt);
   if (mq > 32)
-    return fail(LF_ERR_UNSUPPORTED, "b_q too small: %d query blocks per %d-row tile", mq, rows);
+    return fail(LF_ERR_UNSUPPORTED, "b_q too small: %d query blocks per plan tile", mq);
   g->seg_cap = seg_cap_for(mq, kf * g->bpf, g->list_blocks, a->b_kv);
   g->dense_lo = g->P * a->n;
   g->dense_hi = Lk;
@@ -400,7 +448,7 @@ int past_tiles_estimate(const lf_hsa_args* a, const HsaGeom& g) {
   long long past = total - cur;
   if (past <= 0) return 0;
   past = past < g.cap ? past : g.cap;
-  const long long mq = max_qblocks_per_tile(g.qt, plan_rows());
+  const long long mq = max_qblocks(g.qt);
   long long blocks = mq * past;
   blocks = blocks < g.list_blocks ? blocks : g.list_blocks;
   return (int)((blocks + 1) / 2);
@@ -442,6 +490,9 @@ extern "C" {
 int lf_version(void) { return 100; }
 
 int lf_plan_tile_rows(void) { return plan_rows(); }
+void lf_set_qtile_mode(int32_t mode) { g_qmode_req = mode < 0 ? -1 : mode ? 1 : 0; }
+int lf_qtile_mode(lf_tiling q_tiling) { return qmode_for(q_tiling); }
+int lf_plan_tile_count(lf_tiling q_tiling) { return plan_tile_count(q_tiling); }
 
 int lf_attention_kernel_choice(int32_t heads, int32_t q_rows, int32_t dense_keys,
                                int32_t past_tiles_hint) {
@@ -523,18 +574,25 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
       // contiguous rows: TMA-staged variant (bulk copies of whole blocks)
       if ((d == 128 || d == 64) && q->row_stride == d && k->row_stride == d && q_tiling.block <= 64 &&
           !getenv("LF_POOL_NO_TMA")) {
-        const int tsmem = (d == 128 ? PoolTmaCfg<128>::NST * PoolTmaCfg<128>::STAGE
-                                    : PoolTmaCfg<64>::NST * PoolTmaCfg<64>::STAGE) +
-                          2 * 8 * 4 + smem;
+        // LF_POOL_CFG picks (consumer groups x ring stages): "4x4" (default) or "2x4"
+        const char* pc = getenv("LF_POOL_CFG");
+        const int pcfg = !pc ? LF_POOL_DEFAULT : !strcmp(pc, "4x4") ? 1 : 0;
+#define LF_POOL_LAUNCH(D_, G_, N_)                                                        \
+  do {                                                                                    \
+    using PC = PoolTmaCfg<D_, G_, N_>;                                                    \
+    const int tsmem = PC::NST * PC::STAGE + PC::BAR_BYTES + smem;                         \
+    cudaFuncSetAttribute(pool_frames_tma_kernel<D_, G_, N_>,                              \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);             \
+    pool_frames_tma_kernel<D_, G_, N_><<<grid, PC::THREADS, tsmem, S(stream)>>>(fa);      \
+  } while (0)
         if (d == 128) {
-          cudaFuncSetAttribute(pool_frames_tma_kernel<128>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
-          pool_frames_tma_kernel<128><<<grid, PoolTmaCfg<128>::THREADS, tsmem, S(stream)>>>(fa);
+          if (pcfg == 1) LF_POOL_LAUNCH(128, 4, 4);
+          else LF_POOL_LAUNCH(128, 2, 4);
         } else {
-          cudaFuncSetAttribute(pool_frames_tma_kernel<64>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
-          pool_frames_tma_kernel<64><<<grid, PoolTmaCfg<64>::THREADS, tsmem, S(stream)>>>(fa);
+          if (pcfg == 1) LF_POOL_LAUNCH(64, 4, 4);
+          else LF_POOL_LAUNCH(64, 2, 4);
         }
+#undef LF_POOL_LAUNCH
         return check_launch("pool_frames_tma_kernel");
       }
 #define LF_FP(L)                                                                              \
@@ -662,21 +720,22 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
   if ((rc = check_tiling(k_tiling, "k_tiling"))) return rc;
   if (!seg_count || !segs) return fail(LF_ERR_INVALID, "lf_plan_tiles: null output");
   const int rows = plan_rows();
-  const int ntiles = (q_tiling.total + rows - 1) / rows;
+  const int ntiles = plan_tile_count(q_tiling);
+  const int qmode = qmode_for(q_tiling);
   if (list_blocks <= 0) {
     cudaMemsetAsync(seg_count, 0, (size_t)heads * ntiles * 4, S(stream));
     return check_launch("memset seg_count");
   }
   if (!blocks || !count) return fail(LF_ERR_INVALID, "lf_plan_tiles: null input");
-  if (max_qblocks_per_tile(q_tiling, rows) > 32)
-    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per %d-row tile", rows);
+  if (max_qblocks(q_tiling) > 32)
+    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per plan tile");
   const int spw = list_blocks * 4;
   int wpc = (200 * 1024) / spw;
   if (wpc < 1) return fail(LF_ERR_UNSUPPORTED, "too many key blocks (%d)", list_blocks);
   wpc = wpc > 4 ? 4 : wpc;
   PlanArgs a{blocks, count, heads, nqb, cap, Tiling(q_tiling), Tiling(k_tiling), list_blocks,
-             ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc, rows};
-  if (!getenv("LF_PLAN_WARP")) {
+             ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc, rows, qmode};
+  if (qmode || !getenv("LF_PLAN_WARP")) {  // the warp planner knows 128/256-row tiles only
     if (spw > 48 * 1024)
       cudaFuncSetAttribute(plan_tiles_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, spw);
     plan_tiles_cta_kernel<<<heads * ntiles, 128, spw, S(stream)>>>(a);
@@ -721,8 +780,8 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
         reinterpret_cast<uintptr_t>(m->ptr) % 16)
       return fail(LF_ERR_INVALID, "TMA needs 16-byte aligned rows");
   if (dense_lo < 0 || dense_hi > k->rows) return fail(LF_ERR_INVALID, "dense range outside keys");
-  if (max_qblocks_per_tile(q_tiling, plan_rows()) > 32)
-    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per %d-row tile", plan_rows());
+  if (max_qblocks(q_tiling) > 32)
+    return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per plan tile");
   if (!out) return fail(LF_ERR_INVALID, "null out");
   AttnParams p;
   memset(&p, 0, sizeof(p));
@@ -730,7 +789,8 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
     return rc;
   p.qt = Tiling(q_tiling);
   p.Lq = q->rows;
-  p.n_qtiles = (q->rows + 127) / 128;
+  p.qmode = qmode_for(q_tiling);
+  p.n_qtiles = qtile_count(p.qt, p.qmode);
   p.segs = reinterpret_cast<const int4*>(segs);
   p.seg_count = seg_count;
   p.seg_cap = seg_cap;
@@ -756,6 +816,7 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
     kernel = choose_kernel(q->heads, p.n_qtiles, dense_hi > dense_lo ? dense_hi - dense_lo : 0,
                            past_tiles_hint, sms);
   if (attn_ver()) kernel = attn_ver() == 5 ? LF_KERNEL_PAIR : LF_KERNEL_TILE;
+  if (p.qmode) kernel = LF_KERNEL_TILE;  // the pair kernel has 128-row tiles only
   if (kernel == LF_KERNEL_PAIR) {
     p.tma_out = out_dtype == LF_BF16 && !getenv("LF_ATTN_NO_TMA_OUT") &&
                 make_out_map(&p.to, out, q->d, q->rows, q->heads, out_row_stride, out_head_stride);
@@ -766,6 +827,8 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
 
 size_t lf_hsa_workspace_bytes(const lf_hsa_args* a) {
   HsaGeom g;
+  if (!a) return 0;
+  QmodeScope qs = hsa_qmode_scope(a);
   if (hsa_geom(a, &g)) return 0;
   return carve(g, nullptr).bytes;
 }
@@ -775,6 +838,8 @@ int lf_hsa_views(const lf_hsa_args* a, void* workspace, float** q_block, float**
                  int32_t** budget, int32_t* cap, int32_t* frame_cap) {
   HsaGeom g;
   int rc;
+  if (!a) return fail(LF_ERR_INVALID, "null args");
+  QmodeScope qs = hsa_qmode_scope(a);
   if ((rc = hsa_geom(a, &g))) return rc;
   HsaWs w = carve(g, workspace);
   if (q_block) *q_block = w.q_block;
@@ -793,6 +858,7 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
   HsaGeom g;
   int rc;
   if (!a) return fail(LF_ERR_INVALID, "null args");
+  QmodeScope qs = hsa_qmode_scope(a);
   if ((rc = hsa_geom(a, &g))) return rc;
   HsaWs w = carve(g, workspace);
   if (!workspace || workspace_bytes < w.bytes)

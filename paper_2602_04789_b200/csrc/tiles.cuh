@@ -34,6 +34,7 @@ struct PlanArgs {
   int* seg_count;
   int warps_per_cta;
   int tile_rows;  // 128 or 256
+  int qmode;      // query-tile geometry (qtile_rows): 0 = 128-row, 1 = block-aligned
 };
 
 __global__ void __launch_bounds__(128) plan_tiles_kernel(PlanArgs a) {
@@ -143,9 +144,17 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int w = blockIdx.x;
   const int h = w / a.ntiles, t = w - h * a.ntiles;
-  const int q0 = t * a.tile_rows;
-  int q1 = q0 + a.tile_rows;
-  q1 = q1 < a.qt.total ? q1 : a.qt.total;
+  int q0, q1, mid, xe;
+  if (a.qmode) {  // plan tile t = query tiles 2t, 2t+1
+    qtile_rows(a.qt, 1, 2 * t, q0, mid);
+    if (2 * t + 1 < qtile_count(a.qt, 1)) qtile_rows(a.qt, 1, 2 * t + 1, xe, q1);
+    else q1 = mid;
+  } else {
+    q0 = t * a.tile_rows;
+    q1 = q0 + a.tile_rows;
+    q1 = q1 < a.qt.total ? q1 : a.qt.total;
+    mid = q0 + kTileRows < q1 ? q0 + kTileRows : q1;
+  }
   const int qb0 = a.qt.block_of(q0), qb1 = a.qt.block_of(q1 - 1);
   int any = 0;
   for (int j = tid; j <= qb1 - qb0 && j < 32; j += 128) any |= a.count[h * a.nqb + qb0 + j];
@@ -172,8 +181,7 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
     const unsigned int upto = hi >= 31 ? 0xffffffffu : ((2u << hi) - 1u);
     return upto & ~((1u << lo) - 1u);
   };
-  const bool pairs = a.tile_rows != kTileRows;
-  const int mid = q0 + kTileRows < q1 ? q0 + kTileRows : q1;
+  const bool pairs = a.qmode || a.tile_rows != kTileRows;
   const unsigned int maskA = pairs ? bits(q0, mid) : 0xffffffffu;
   const unsigned int maskB = pairs ? bits(mid, q1) : 0u;
   // this warp's key-block range

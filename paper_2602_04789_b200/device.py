@@ -7,8 +7,10 @@ attention.py, planner.py, numerics.py in this package) is built on these.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -22,6 +24,62 @@ TILE_ROWS = 128  # query rows per tcgen05 tile (one TMEM lane each)
 def plan_rows() -> int:
     """Rows per tile plan: 256 (a pair of 128-row query tiles) unless the legacy kernel is selected."""
     return int(L.lib().lf_plan_tile_rows())
+
+
+_qmode_req = -1
+
+
+def set_qtile_mode(mode: int) -> None:
+    """Query-tile geometry for later plans and attention calls: 1 = block-aligned
+    (two query blocks per tensor-core tile), 0 = 128-row tiles, -1 = automatic
+    (LF_QTILE env when set, else chosen per step by the rollout / pipeline)."""
+    global _qmode_req
+    _qmode_req = -1 if mode < 0 else int(mode)
+    L.lib().lf_set_qtile_mode(_qmode_req)
+
+
+BLOCK_TILES_MIN_PAST = 16  # csrc/lfattn.cu kBlockTilesMinPast
+
+
+def auto_qtile_mode(s_host, chunk: int, f: int, bpf: int, topk_frames: int) -> int:
+    """Geometry for one step from the host s_i (mirrors auto_qmode in lfattn.cu):
+    block-aligned tiles when the estimated past blocks per query block is >= 16
+    and below all past blocks (a fully selected past gives every block one list)."""
+    P = (chunk - 1) * f
+    if P <= 0 or s_host is None or not (0.0 <= float(s_host) < 1.0):
+        return 0
+    cur = f * bpf
+    past = min(int((1.0 - float(s_host)) * chunk * cur + 0.5) - cur, min(topk_frames, P) * bpf)
+    return 1 if BLOCK_TILES_MIN_PAST <= past < P * bpf else 0
+
+
+@contextlib.contextmanager
+def qtile_scope(mode: int):
+    """Plans and attention calls inside use query-tile geometry `mode` (an
+    explicit LF_QTILE environment setting still wins)."""
+    if _qmode_req >= 0 or os.environ.get("LF_QTILE"):
+        yield  # an explicit choice wins
+        return
+    L.lib().lf_set_qtile_mode(int(mode))
+    try:
+        yield
+    finally:
+        L.lib().lf_set_qtile_mode(-1)
+
+
+def qtile_mode(qt) -> int:
+    """The query-tile geometry the library uses for this query tiling."""
+    return int(L.lib().lf_qtile_mode(qt.abi()))
+
+
+def qtile_rows(qt, mode: int, t: int):
+    """Rows [x0, x1) of query tile t (csrc/common.cuh qtile_rows)."""
+    if mode:
+        nb = qt.count
+        x0 = qt.block_start(2 * t)
+        x1 = qt.block_start(2 * t + 2) if 2 * t + 2 < nb else qt.total
+        return x0, x1
+    return t * TILE_ROWS, min(t * TILE_ROWS + TILE_ROWS, qt.total)
 
 
 def _dev():
@@ -57,6 +115,10 @@ class TilingSpec:
         s = t * self.period + j * self.block
         e = np.minimum(np.minimum(s + self.block, t * self.period + self.period), self.total)
         return np.stack([s, e], axis=1)
+
+    def block_start(self, g: int) -> int:
+        t, j = divmod(g, self.per_period)
+        return t * self.period + j * self.block
 
     def max_blocks_per_tile(self, rows: int = TILE_ROWS) -> int:
         worst = 0
@@ -181,10 +243,11 @@ def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
     lib = L.lib()
     H, nqb, cap = blocks.shape
     rows = plan_rows()
-    ntiles = -(-qt.total // rows)
+    ntiles = int(lib.lf_plan_tile_count(qt.abi()))
+    mq = 4 if qtile_mode(qt) else qt.max_blocks_per_tile(rows)
     pieces = -(-kt.block // SEG_KEYS)
     if seg_cap is None:
-        seg_cap = max(1, min(qt.max_blocks_per_tile(rows) * cap * pieces, max(list_blocks, 0) * pieces)
+        seg_cap = max(1, min(mq * cap * pieces, max(list_blocks, 0) * pieces)
                       + (3 if rows > TILE_ROWS else 0))
     dev = blocks.device
     segs = torch.empty((H, ntiles, seg_cap, 4), dtype=torch.int32, device=dev)

@@ -103,8 +103,8 @@ class HsaPipeline:
         L.check(lib.lf_hsa_forward(ctypes.byref(self._args), self._ws.data_ptr(),
                                    self._ws.numel(), L.stream_ptr()))
 
-    def __call__(self, q, k, v, s_i, out=None):
-        out = self.bind(q, k, v, s_i, out)
+    def __call__(self, q, k, v, s_i, out=None, s_host=None):
+        out = self.bind(q, k, v, s_i, out, s_host=s_host)
         self.launch()
         return out
 

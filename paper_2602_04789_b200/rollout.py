@@ -166,15 +166,18 @@ class HsaRollout:
         s_dev = self._s_dev(i, s_i)
         sel = D.select(q_block, self.kb_cache, self.kf_cache, self.bpf, i, lay.f,
                        self.cfg.topk_frames, self.cfg.block_budget_mode == "per-frame", s_dev)
-        tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * self.bpf)
         if s_host is None and s_i is not None and not torch.is_tensor(s_i):
             s_host = float(s_i)
         if s_host is None and s_i is None and self.plan is not None:
             s_host = float(self.plan.s[i - 1])
+        # query-tile geometry of this step (block-aligned when the past selection is large)
+        with D.qtile_scope(D.auto_qtile_mode(s_host, i, lay.f, self.bpf, self.cfg.topk_frames)):
+            tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * self.bpf)
+            qmode = D.qtile_mode(qt)
         hint = D.past_tiles_hint(s_host, i, lay.f, self.bpf, self.cfg.topk_frames, qt)
         self.last_selection = sel
         self.last_chunk = i
-        return StepPlan(q, i, qt, q_block, sel, tiles, hint)
+        return StepPlan(q, i, qt, q_block, sel, tiles, hint, qmode)
 
     def attend(self, plan: "StepPlan", out: torch.Tensor | None = None) -> torch.Tensor:
         """Attention half of a step: block-sparse attention of plan.q over the
@@ -183,15 +186,16 @@ class HsaRollout:
         i = plan.chunk
         P = (i - 1) * lay.f
         lk = lay.context_tokens(i)
-        return D.attention(plan.q, self.kv_k[:, :lk], self.kv_v[:, :lk], plan.qt, plan.tiles,
-                           P * lay.n, lk, out=out, out_dtype=self.out_dtype,
-                           scale=1.0 / math.sqrt(lay.d), err=self.err, past_tiles=plan.hint)
+        with D.qtile_scope(plan.qmode):
+            return D.attention(plan.q, self.kv_k[:, :lk], self.kv_v[:, :lk], plan.qt, plan.tiles,
+                               P * lay.n, lk, out=out, out_dtype=self.out_dtype,
+                               scale=1.0 / math.sqrt(lay.d), err=self.err, past_tiles=plan.hint)
 
 
 class StepPlan:
     """Device results of HsaRollout.prepare (kept alive until attend has run)."""
 
-    def __init__(self, q, chunk, qt, q_block, selection, tiles, hint):
+    def __init__(self, q, chunk, qt, q_block, selection, tiles, hint, qmode=0):
         self.q = q
         self.chunk = chunk
         self.qt = qt
@@ -199,6 +203,7 @@ class StepPlan:
         self.selection = selection
         self.tiles = tiles
         self.hint = hint
+        self.qmode = qmode  # query-tile geometry the plan was made for (device.qtile_rows)
 
 
 # --------------------------------------------------------------------------- ablation settings

@@ -1,6 +1,8 @@
-for nst in 3 6 8; do
-  touch paper_2602_04789_b200/csrc/lfattn.cu
-  LF_NVCC_FLAGS="-DLF_POOL_NST=$nst" python -c "import __graft_entry__ as g; g.build()" > /dev/null
-  timeout 300 python bench.py --config c2 --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/pool_nst$nst.json 2>/dev/null
-  python -c "import json;d=json.load(open('gpurun_out/pool_nst$nst.json'));s=d['roofline_select'];print('NST $nst', round(s['achieved']), round(s['pool_ms_per_call']*1e3,1))"
+# A/B of the pooling kernel's (consumer groups x ring stages) at c2 and c5_dense (run via gpurun)
+python -c "import __graft_entry__ as g; g.build()" > /dev/null
+for cfg in 2x4 4x4 2x4 4x4; do
+  for c in c2 c3; do
+    LF_POOL_CFG=$cfg timeout 300 python bench.py --config $c --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/pool_${cfg}_$c.json 2>gpurun_out/pool_${cfg}_$c.err
+    python -c "import json;d=json.load(open('gpurun_out/pool_${cfg}_$c.json'));s=d['roofline_select'];print('$cfg $c', round(s['achieved']), round(s['frac'],3), round(s['pool_ms_per_call']*1e3,1), 'headline', round(d['value']))"
+  done
 done

@@ -60,8 +60,11 @@ def test_topk_indices(lf):
         assert got.tolist() == c["indices"], c
 
 
+@pytest.mark.parametrize("pool_cfg", ["2x4", "4x4"])
 @pytest.mark.parametrize("kind", ["aligned", "framewise"])
-def test_compress_bit_exact(lf, kind):
+def test_compress_bit_exact(lf, kind, pool_cfg, monkeypatch):
+    # every (consumer groups x ring stages) variant of the TMA pooling kernel
+    monkeypatch.setenv("LF_POOL_CFG", pool_cfg)
     for m, arr in hsa_cases(kind):
         c = m["case"]
         if f"qb{c}" not in arr:

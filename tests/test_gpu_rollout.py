@@ -33,7 +33,8 @@ def test_rollout_cache_matches_pipeline_and_oracle(n, f, d, N, topk, plan):
         vfull = np.concatenate([clean[t][2] for t in range(i - 1)] + [vc], axis=1)
         kd, vd = (torch.from_numpy(a).to(dev, torch.bfloat16) for a in (kfull, vfull))
         pipe = lf.HsaPipeline(lay, H, i, cfg, framewise=fw, out_dtype=torch.float32)
-        ref_gpu = pipe(qd, kd, vd, pl.s_device(i)).cpu().numpy()
+        # s_host: both paths then pick the same query-tile geometry (bit-equal outputs)
+        ref_gpu = pipe(qd, kd, vd, pl.s_device(i), s_host=float(pl.s[i - 1])).cpu().numpy()
         np.testing.assert_array_equal(out, ref_gpu)
         masks = pipe.masks()
         for h in range(H):
