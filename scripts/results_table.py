@@ -12,9 +12,10 @@ for f in sorted(glob.glob(os.path.join(rd, "bench_c*.json"))):
     rows.append((d["config"]["workload"].split(":")[0], d["value"], d["ms_per_chunk"], e["value"],
                  e.get("ms_per_chunk"), e.get("pcie_bound_ms_per_chunk"),
                  r["kernel"].split("<")[0], r["achieved"], r["frac"], r["attn_ms_per_call"] * 1e3,
-                 s["achieved"], s["frac"], s["select_plan_ms_per_call"] * 1e3))
-print("| config | headline TFLOP/s | ms/chunk | e2e TFLOP/s (ms/chunk, PCIe bound) | attention kernel | attn TFLOP/s (frac) | attn µs/call | pool GB/s (frac) | select+plan µs/call |")
+                 s["achieved"], s["frac"], s["select_plan_ms_per_call"] * 1e3,
+                 d["config"].get("query_tiles", "128-row").split(" (")[0]))
+print("| config | headline TFLOP/s | ms/chunk | e2e TFLOP/s (ms/chunk, PCIe bound) | query tiles | attn TFLOP/s (frac) | attn µs/call | pool GB/s (frac) | select+plan µs/call |")
 print("|---|---|---|---|---|---|---|---|---|")
-for c, v, ms, ev, ems, pb, k, a, fr, au, pg, pf, su in rows:
-    print(f"| {c} | {v:.0f} | {ms:.3f} | {ev:.0f} ({ems:.2f}, {pb:.2f}) | {k} | {a:.0f} ({fr:.3f}) | {au:.0f} | "
+for c, v, ms, ev, ems, pb, k, a, fr, au, pg, pf, su, qt in rows:
+    print(f"| {c} | {v:.0f} | {ms:.3f} | {ev:.0f} ({ems:.2f}, {pb:.2f}) | {qt} | {a:.0f} ({fr:.3f}) | {au:.0f} | "
           f"{pg:.0f} ({pf:.2f}) | {su:.0f} |")
