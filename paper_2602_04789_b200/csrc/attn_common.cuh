@@ -46,6 +46,8 @@ struct AttnParams {
   float* part_o;    // split partials (tile kernel: fp32 [part][128][D]; pair kernel: fp16 O/l)
   float2* part_ml;  // [part][rows] (row max, row sum)
   int* counters;    // [tail], zero between launches
+  int* sched;       // tile kernel: [2] next unit + finished CTAs, zero between launches;
+                    // null: static round-robin units
 };
 
 struct TileSegs {

@@ -43,7 +43,7 @@ struct AttnCfg7 {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + VST * KV_BYTES;
-  static constexpr int OFF_STAT = OFF_BAR + 256;  // float2 [2 sets][128 rows]
+  static constexpr int OFF_STAT = OFF_BAR + 512;  // float2 [2 sets][128 rows]
   static constexpr int SMEM = OFF_STAT + 2 * 128 * 8 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
   static constexpr int TMEM_COLS = 512;
@@ -88,6 +88,29 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
   int* flag = reinterpret_cast<int*>(bars + 27);
   static_assert(C::KST <= 4 && C::VST <= 4, "barrier slots");
+  // dynamic item schedule (p.sched): the producer warp fetches the next unit
+  // from a global counter when it is ready for its Q and publishes the unit id
+  // through a 4-slot ring to the MMA warp and the 8 softmax warps; null sched:
+  // static round-robin (unit blockIdx.x + k * gridDim.x)
+  constexpr int IR = 4;
+  uint64_t* it_full = bars + 32;   // [IR]
+  uint64_t* it_empty = bars + 36;  // [IR]
+  int* it_ids = reinterpret_cast<int*>(bars + 40);
+  const bool dyn = p.sched != nullptr;
+  auto next_static = [&](int it) -> int {
+    const int w = (int)blockIdx.x + it * (int)gridDim.x;
+    return w < total_work ? w : -1;
+  };
+  // consumer side: unit of the it-th item of this CTA (-1: done)
+  auto take_item = [&](int it) -> int {
+    if (!dyn) return next_static(it);
+    const int sl = it % IR;
+    mbar_wait(it_full + sl, (it / IR) & 1);
+    const int w = it_ids[sl];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(it_empty + sl);
+    return w;
+  };
   float2* stat = reinterpret_cast<float2*>(smem + C::OFF_STAT);
 
   const int warp = threadIdx.x >> 5;
@@ -110,6 +133,10 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(v_full + b, 1);
       mbar_init(v_empty + b, 1);
     }
+    for (int i = 0; i < IR; ++i) {
+      mbar_init(it_full + i, 1);
+      mbar_init(it_empty + i, 9);  // MMA warp + 8 softmax warps
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -127,7 +154,24 @@ __global__ void __launch_bounds__(320, 1)
     }
     __syncwarp();
     uint32_t kit = 0, nq = 0;
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+    for (int it = 0;; ++it) {
+      int w;
+      if (dyn) {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(p.sched, 1);
+        v = __shfl_sync(0xffffffffu, v, 0);
+        w = v < total_work ? v : -1;
+        const int sl = it % IR;
+        mbar_wait(it_empty + sl, ((it / IR) & 1) ^ 1);
+        if (lane == 0) {
+          it_ids[sl] = w;
+          mbar_arrive(it_full + sl);
+        }
+        __syncwarp();
+      } else {
+        w = next_static(it);
+      }
+      if (w < 0) break;
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
@@ -171,6 +215,15 @@ __global__ void __launch_bounds__(320, 1)
         ++kit;
       }
     }
+    // the last CTA past its final fetch resets the schedule for the next launch
+    if (dyn && lane == 0) {
+      __threadfence();
+      if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
+        __threadfence();
+      }
+    }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
     constexpr uint32_t IDESC_QK = idesc_bf16(128, 128, 0, 0);
@@ -179,7 +232,9 @@ __global__ void __launch_bounds__(320, 1)
     const uint64_t kd0 = smem_desc_sw128(smem_u32(sK), 16, 1024);
     const uint64_t vd0 = smem_desc_sw128(smem_u32(sV), C::BN * 128, 1024);
     uint32_t kit = 0, nq = 0, np[2] = {0, 0}, noe = 0;
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+    for (int it = 0;; ++it) {
+      const int w = take_item(it);
+      if (w < 0) break;
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
@@ -273,7 +328,9 @@ __global__ void __launch_bounds__(320, 1)
     const float c2 = p.scale_log2;
     uint32_t ns = 0, no = 0, nitem = 0;
     const bool tr = (warp == 2 || warp == 6) && lane == 0;  // one thread per set
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x, ++nitem) {
+    for (int it = 0;; ++it, ++nitem) {
+      const int w = take_item(it);
+      if (w < 0) break;
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       const int grow = cx.x0 + row;

@@ -360,11 +360,23 @@ int launch_v3(AttnParams& p, int heads, int d, int sms, void* stream) {
     rem = items;
   }
   if (tail_split < 2) { rem = 0; tail_split = 1; }
-  if (rem > 0) {
-    const size_t need_c = align_up((size_t)rem * 4, 256);
-    const size_t need_ml = align_up((size_t)rem * tail_split * 128 * 8, 256);
-    const size_t need_o = (size_t)rem * tail_split * 128 * d * 4;
-    if (!split_scratch(need_c, need_ml, need_o, S(stream), &p.counters, &p.part_ml, &p.part_o)) {
+  // counters region: [8 ints: the dynamic schedule][rem tail counters]
+  // dynamic schedule for sparse plans (block-aligned geometry), where items
+  // differ in key-tile count: attention -2 % at c3, -4 % at c5_s70; static
+  // round-robin for dense-like plans (+2 % slower dynamic at c5_dense).
+  // LF_ATTN_STATIC=1 / LF_ATTN_DYNAMIC=1 force one (profiles/r01/sched_ab.txt).
+  const bool dyn = getenv("LF_ATTN_DYNAMIC") ? true : getenv("LF_ATTN_STATIC") ? false : p.qmode == 1;
+  {
+    const int nr = rem > 0 ? rem : 0;
+    const size_t need_c = align_up((size_t)(nr + 8) * 4, 256);
+    const size_t need_ml = align_up((size_t)nr * tail_split * 128 * 8, 256);
+    const size_t need_o = (size_t)nr * tail_split * 128 * d * 4;
+    int* base = nullptr;
+    if (split_scratch(need_c, need_ml, need_o, S(stream), &base, &p.part_ml, &p.part_o)) {
+      p.sched = dyn ? base : nullptr;
+      p.counters = base + 8;
+    } else {
+      p.sched = nullptr;
       rem = 0;
       tail_split = 1;
     }

@@ -92,3 +92,38 @@ def test_block_tiles_config2_shape(lf):
 
 def test_block_tiles_rollout(lf):
     test_gpu_rollout.test_rollout_cache_matches_pipeline_and_oracle(1560, 3, 128, 5, 6, (0.3, 0.6))
+
+
+# ---------------------------------------------------------------- dynamic schedule
+# The tile kernel fetches units from a global counter (reset by the last CTA)
+# for block-aligned plans; the result must not depend on which CTA ran a unit.
+
+@pytest.mark.parametrize("split", [None, "3"])
+def test_dynamic_schedule_vs_oracle(lf, split, monkeypatch):
+    monkeypatch.setenv("LF_ATTN_DYNAMIC", "1")
+    if split:
+        monkeypatch.setenv("LF_ATTN_SPLIT", split)
+    _pipeline_case(lf, 3, 1560, 3, 5, 128, 0.6, 6, "global", seed=55, check_heads=(0, 2))
+
+
+def test_dynamic_schedule_graph_replay(lf, monkeypatch):
+    monkeypatch.setenv("LF_ATTN_DYNAMIC", "1")
+    lay = lf.ChunkLayout(f=3, n=1560, b_q=64, b_kv=64, d=128, N=7)
+    H, i = 5, 6
+    q, k, v = O.synthetic_qkv(6, 3 * 1560, i * 3 * 1560, 128, heads=H)
+    dev = torch.device("cuda")
+    qd, kd, vd = (torch.from_numpy(a).to(dev, torch.bfloat16) for a in (q, k, v))
+    pipe = lf.HsaPipeline(lay, H, i, lf.SelectionConfig(), framewise=True)
+    out = pipe.bind(qd, kd, vd, 0.5)
+    pipe.launch()
+    first = out.clone()
+    pipe.capture()
+    for _ in range(4):  # the unit counter must be back at zero after every launch
+        pipe.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(first, out)
+    monkeypatch.setenv("LF_ATTN_STATIC", "1")
+    monkeypatch.delenv("LF_ATTN_DYNAMIC")
+    pipe.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(first, out)  # static round-robin: same result
