@@ -31,3 +31,20 @@ def test_block_aligned_rows_cover_the_chunk():
         # tile boundaries are block boundaries
         starts = {int(s) for s, _ in qt.bounds()}
         assert all(x0 in starts for x0, _ in rows)
+
+
+def test_c_abi_geometry_queries_on_host():
+    # host-only entry points (no device work): forced mode, tile counts, eligibility
+    from paper_2602_04789_b200 import _lib as L
+    lib = L.load_library()  # no device needed for these
+    qt = D.TilingSpec(3 * 1560, 1560, 64)
+    try:
+        lib.lf_set_qtile_mode(1)
+        assert lib.lf_qtile_mode(qt.abi()) == 1
+        assert lib.lf_plan_tile_count(qt.abi()) == -(-qt.count // 4)  # 75 blocks -> 19
+        assert lib.lf_qtile_mode(D.TilingSpec(1024, 1024, 128).abi()) == 0
+        lib.lf_set_qtile_mode(0)
+        assert lib.lf_qtile_mode(qt.abi()) == 0
+        assert lib.lf_plan_tile_count(qt.abi()) == -(-qt.total // 256)
+    finally:
+        lib.lf_set_qtile_mode(-1)
