@@ -115,6 +115,18 @@ int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f,
                 double* alpha, double* s, int32_t* budgets, int32_t* clamped, double* scalars,
                 int32_t* status, void* stream);
 
+/* Summaries of one committed clean chunk for an incremental key-summary cache
+ * (the rollout caller, rollout.py:306-308; selection.py:109-113 per frame):
+ * k [H][f*n][d] bf16 with contiguous rows (d 64 or 128, blocks <= 64 rows,
+ * k_tiling = the chunk's frames) -> its block means into k_block
+ * ([H][f*bpf][d] fp32 rows at kb_head_stride elements per head) and its frame
+ * summaries into k_frame ([H][f][d] at kf_head_stride), in one launch,
+ * bit-identical to lf_compress.  LF_ERR_UNSUPPORTED for other layouts (use
+ * lf_pool_blocks twice). */
+int lf_pool_chunk_k(const lf_mat* k, lf_tiling k_tiling, int32_t blocks_per_frame,
+                    float* k_block, int64_t kb_head_stride, float* k_frame,
+                    int64_t kf_head_stride, void* stream);
+
 /* Rows per tile plan (lf_plan_tile_rows(): 256 = a pair of 128-row query
  * tiles; both attention kernels read these plans). */
 int lf_plan_tile_rows(void);

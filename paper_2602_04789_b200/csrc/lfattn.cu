@@ -102,6 +102,30 @@ int check_tiling(lf_tiling t, const char* name) {
   return LF_OK;
 }
 
+// K1 launch (pool.cuh pool_frames_tma_kernel): contiguous bf16 rows, d 64/128,
+// blocks <= 64 rows. LF_POOL_CFG picks (consumer groups x ring stages):
+// "4x4" (default) or "2x4".
+void launch_frame_pool_tma(const FramePoolArgs& fa, int d, int smem, int grid, void* stream) {
+  const char* pc = getenv("LF_POOL_CFG");
+  const int pcfg = !pc ? LF_POOL_DEFAULT : !strcmp(pc, "4x4") ? 1 : 0;
+#define LF_POOL_LAUNCH(D_, G_, N_)                                                        \
+  do {                                                                                    \
+    using PC = PoolTmaCfg<D_, G_, N_>;                                                    \
+    const int tsmem = PC::NST * PC::STAGE + PC::BAR_BYTES + smem;                         \
+    cudaFuncSetAttribute(pool_frames_tma_kernel<D_, G_, N_>,                              \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);             \
+    pool_frames_tma_kernel<D_, G_, N_><<<grid, PC::THREADS, tsmem, S(stream)>>>(fa);      \
+  } while (0)
+  if (d == 128) {
+    if (pcfg == 1) LF_POOL_LAUNCH(128, 4, 4);
+    else LF_POOL_LAUNCH(128, 2, 4);
+  } else {
+    if (pcfg == 1) LF_POOL_LAUNCH(64, 4, 4);
+    else LF_POOL_LAUNCH(64, 2, 4);
+  }
+#undef LF_POOL_LAUNCH
+}
+
 // ---- pooling dispatch
 template <typename T>
 int launch_pool_t(const PoolArgs& a, int vec, int ns, cudaStream_t st) {
@@ -581,30 +605,14 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
       fa.k_frames = k_tiling.total / k_tiling.period;
       fa.past_frames = past_frames;
       fa.q_block = q_block; fa.k_block = k_block; fa.k_frame = k_frame;
+      fa.kb_head = (long long)fa.k_frames * per * d;
+      fa.kf_head = (long long)past_frames * d;
       const int smem = per * d * 4;
       const int grid = q->heads * (fa.q_frames + fa.k_frames);
       // contiguous rows: TMA-staged variant (bulk copies of whole blocks)
       if ((d == 128 || d == 64) && q->row_stride == d && k->row_stride == d && q_tiling.block <= 64 &&
           !getenv("LF_POOL_NO_TMA")) {
-        // LF_POOL_CFG picks (consumer groups x ring stages): "4x4" (default) or "2x4"
-        const char* pc = getenv("LF_POOL_CFG");
-        const int pcfg = !pc ? LF_POOL_DEFAULT : !strcmp(pc, "4x4") ? 1 : 0;
-#define LF_POOL_LAUNCH(D_, G_, N_)                                                        \
-  do {                                                                                    \
-    using PC = PoolTmaCfg<D_, G_, N_>;                                                    \
-    const int tsmem = PC::NST * PC::STAGE + PC::BAR_BYTES + smem;                         \
-    cudaFuncSetAttribute(pool_frames_tma_kernel<D_, G_, N_>,                              \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);             \
-    pool_frames_tma_kernel<D_, G_, N_><<<grid, PC::THREADS, tsmem, S(stream)>>>(fa);      \
-  } while (0)
-        if (d == 128) {
-          if (pcfg == 1) LF_POOL_LAUNCH(128, 4, 4);
-          else LF_POOL_LAUNCH(128, 2, 4);
-        } else {
-          if (pcfg == 1) LF_POOL_LAUNCH(64, 4, 4);
-          else LF_POOL_LAUNCH(64, 2, 4);
-        }
-#undef LF_POOL_LAUNCH
+        launch_frame_pool_tma(fa, d, smem, grid, stream);
         return check_launch("pool_frames_tma_kernel");
       }
 #define LF_FP(L)                                                                              \
@@ -647,6 +655,36 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
     if ((rc = launch_pool(b, LF_F32, vf, nf, S(stream)))) return rc;
   }
   return LF_OK;
+}
+
+int lf_pool_chunk_k(const lf_mat* k, lf_tiling k_tiling, int32_t blocks_per_frame,
+                    float* k_block, int64_t kb_head_stride, float* k_frame,
+                    int64_t kf_head_stride, void* stream) {
+  int rc;
+  if ((rc = check_mat(k, "k")) || (rc = check_tiling(k_tiling, "k_tiling"))) return rc;
+  if (!k_block || !k_frame) return fail(LF_ERR_INVALID, "lf_pool_chunk_k: null output");
+  const int d = k->d;
+  const int per = (k_tiling.period + k_tiling.block - 1) / k_tiling.block;
+  if (k->dtype != LF_BF16 || (d != 64 && d != 128) || k->row_stride != d ||
+      k->head_stride % 8 || reinterpret_cast<uintptr_t>(k->ptr) % 16 || k_tiling.block > 64 ||
+      k_tiling.total != k->rows || k_tiling.total % k_tiling.period || per != blocks_per_frame ||
+      (size_t)per * d * 4 > 96 * 1024)
+    return fail(LF_ERR_UNSUPPORTED, "lf_pool_chunk_k: needs contiguous bf16 rows, d 64/128, "
+                                    "whole frames, blocks <= 64 rows");
+  FramePoolArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.k = static_cast<const __nv_bfloat16*>(k->ptr);
+  fa.k_row = k->row_stride; fa.k_head = k->head_stride;
+  fa.heads = k->heads; fa.d = d; fa.period = k_tiling.period; fa.block = k_tiling.block;
+  fa.per_period = per;
+  fa.q_frames = 0;
+  fa.k_frames = k_tiling.total / k_tiling.period;
+  fa.past_frames = fa.k_frames;  // every frame of a committed chunk is a past frame
+  fa.k_block = k_block; fa.k_frame = k_frame;
+  fa.kb_head = kb_head_stride;
+  fa.kf_head = kf_head_stride;
+  launch_frame_pool_tma(fa, d, per * d * 4, k->heads * fa.k_frames, stream);
+  return check_launch("pool_frames_tma_kernel");
 }
 
 static int select_smem_per_warp(int d, int P, int frame_cap, int max_cand) {

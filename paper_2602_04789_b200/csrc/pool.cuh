@@ -171,6 +171,7 @@ struct FramePoolArgs {
   float* q_block;  // [H][q_frames*bpf][d]
   float* k_block;  // [H][k_frames*bpf][d]
   float* k_frame;  // [H][past_frames][d]
+  long long kb_head, kf_head;  // head strides (elements) of k_block / k_frame
 };
 
 __device__ __forceinline__ double bf16_hi_scaled(uint32_t w) {
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(512) pool_frames_bf16_kernel(FramePoolArgs a) 
       is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
   const long long rs = is_q ? a.q_row : a.k_row;
   float* out = is_q ? a.q_block + ((long long)h * a.q_frames * a.per_period) * a.d
-                    : a.k_block + ((long long)h * a.k_frames * a.per_period) * a.d;
+                    : a.k_block + (long long)h * a.kb_head;
   const int grp = threadIdx.x / LPB;
   const int gl = threadIdx.x - grp * LPB;
   const int col = gl * 8;
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(512) pool_frames_bf16_kernel(FramePoolArgs a) 
   if (!keep) return;
   __syncthreads();
   // k_frame = mean_pool(k_block, bpf): fp64 in block order, / bpf, -> fp32
-  float* kf = a.k_frame + ((long long)h * a.past_frames + frame) * a.d;
+  float* kf = a.k_frame + (long long)h * a.kf_head + (long long)frame * a.d;
   for (int c = threadIdx.x; c < a.d; c += blockDim.x) {
     double s = (double)fp_smem[c];
     for (int j = 1; j < a.per_period; ++j) s += (double)fp_smem[j * a.d + c];
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frame
   const int frame = is_q ? fr : fr - a.q_frames;
   const __nv_bfloat16* base = is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
   float* out = is_q ? a.q_block + ((long long)h * a.q_frames * a.per_period) * D
-                    : a.k_block + ((long long)h * a.k_frames * a.per_period) * D;
+                    : a.k_block + (long long)h * a.kb_head;
   const bool keep = !is_q && frame < a.past_frames;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frame
   }
   if (!keep) return;
   asm volatile("bar.sync 1, %0;" ::"r"(G * D / 2) : "memory");  // consumer threads only
-  float* kf = a.k_frame + ((long long)h * a.past_frames + frame) * D;
+  float* kf = a.k_frame + (long long)h * a.kf_head + (long long)frame * D;
   for (int cc = t; cc < D; cc += G * D / 2) {
     double s = (double)fp_smem[cc];
     for (int j = 1; j < a.per_period; ++j) s += (double)fp_smem[j * D + cc];

@@ -103,10 +103,14 @@ class HsaRollout:
                             lay.b_kv)
         nb = lay.f * self.bpf
         kb = self.kb_cache[:, (i - 1) * nb:i * nb]
-        self._pool_into(self.kv_k[:, sl], spec, kb)
-        # k_frame rows = mean of each frame's block means (selection.py:111)
-        fspec = D.TilingSpec(nb, nb, self.bpf)
-        self._pool_into(kb, fspec, self.kf_cache[:, (i - 1) * lay.f:i * lay.f])
+        kf = self.kf_cache[:, (i - 1) * lay.f:i * lay.f]
+        # one launch (block means + frame summaries, lf_pool_chunk_k) when the
+        # layout allows it, else two pooling passes; both bit-identical
+        if not (self.framewise and self._pool_chunk(self.kv_k[:, sl], spec, kb, kf)):
+            self._pool_into(self.kv_k[:, sl], spec, kb)
+            # k_frame rows = mean of each frame's block means (selection.py:111)
+            fspec = D.TilingSpec(nb, nb, self.bpf)
+            self._pool_into(kb, fspec, kf)
         self.committed = max(self.committed, i)
 
     def selection_flops(self) -> int:
@@ -124,6 +128,18 @@ class HsaRollout:
             for r in range(qt.count):
                 total += int(rows[r]) * (cur + int(cols[b[h, r, :c[h, r]]].sum()))
         return int(4 * self.layout.d * total)
+
+    def _pool_chunk(self, x, spec: D.TilingSpec, kb, kf) -> bool:
+        import ctypes
+
+        from . import _lib as L
+        m = L.mat(x)
+        rc = L.lib().lf_pool_chunk_k(ctypes.byref(m), spec.abi(), self.bpf, kb.data_ptr(),
+                                     kb.stride(0), kf.data_ptr(), kf.stride(0), L.stream_ptr())
+        if rc == L.LF_ERR_UNSUPPORTED:
+            return False
+        L.check(rc)
+        return True
 
     def _pool_into(self, x: torch.Tensor, spec: D.TilingSpec, out: torch.Tensor) -> None:
         import ctypes
