@@ -248,3 +248,33 @@ def test_split_kv_merge(lf, split, monkeypatch):
     out = lf.dense_attention(q[0], k[0], v[0])
     assert_close_attn(out, O.dense_attention(q[0], k[0], v[0]), f"split {split}")
     _pipeline_case(lf, 3, 1560, 3, 4, 128, 0.5, 6, "global", seed=4, check_heads=(1,))
+
+
+@pytest.mark.parametrize("H,f,n,d", [(3, 3, 1560, 128), (2, 2, 256, 64)])
+def test_pool_chunk_k_matches_compress(lf, H, f, n, d):
+    # lf_pool_chunk_k (one launch, strided outputs into a cache) == lf_compress bit for bit
+    import ctypes
+    from paper_2602_04789_b200 import _lib as L, device as D
+    dev = torch.device("cuda")
+    L_ = f * n
+    _, k, _ = O.synthetic_qkv(H * 7 + n, L_, L_, d, heads=H)
+    kd = torch.from_numpy(k).to(dev, torch.bfloat16)
+    kt = D.TilingSpec(L_, n, 64)
+    bpf = -(-n // 64)
+    _, kb_ref, kf_ref = D.compress(kd, kd, kt, kt, bpf, f)
+    # outputs land in the middle of larger caches (head strides != dense)
+    kb_cache = torch.full((H, 3 * f * bpf, d), 7.0, device=dev)
+    kf_cache = torch.full((H, 3 * f, d), 7.0, device=dev)
+    kb, kf = kb_cache[:, f * bpf:2 * f * bpf], kf_cache[:, f:2 * f]
+    m = L.mat(kd)
+    L.check(L.lib().lf_pool_chunk_k(ctypes.byref(m), kt.abi(), bpf, kb.data_ptr(), kb.stride(0),
+                                    kf.data_ptr(), kf.stride(0), L.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(kb, kb_ref) and torch.equal(kf, kf_ref)
+    assert torch.all(kb_cache[:, :f * bpf] == 7.0) and torch.all(kf_cache[:, 2 * f:] == 7.0)
+    # a layout the one-launch path does not take reports UNSUPPORTED (callers pool twice)
+    k32 = torch.from_numpy(k).to(dev)
+    m32 = L.mat(k32)
+    rc = L.lib().lf_pool_chunk_k(ctypes.byref(m32), kt.abi(), bpf, kb.data_ptr(), kb.stride(0),
+                                 kf.data_ptr(), kf.stride(0), L.stream_ptr())
+    assert rc == L.LF_ERR_UNSUPPORTED
