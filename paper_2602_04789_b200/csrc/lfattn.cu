@@ -107,7 +107,12 @@ int check_tiling(lf_tiling t, const char* name) {
 // "4x4" (default) or "2x4".
 void launch_frame_pool_tma(const FramePoolArgs& fa, int d, int smem, int grid, void* stream) {
   const char* pc = getenv("LF_POOL_CFG");
-  const int pcfg = !pc ? LF_POOL_DEFAULT : !strcmp(pc, "4x4") ? 1 : 0;
+  int pcfg = !pc ? LF_POOL_DEFAULT : !strcmp(pc, "4x4") ? 1 : !strcmp(pc, "4x8") ? 2 : 0;
+  // fewer CTAs than SMs (a single chunk commit: H*f CTAs): one CTA per SM and
+  // the frame's blocks are the critical path, so 8 consumer groups (8 blocks
+  // summed at once) over an 8-stage ring
+  if (!pc && grid < 148) pcfg = 3;
+  if (pc && !strcmp(pc, "8x8")) pcfg = 3;
 #define LF_POOL_LAUNCH(D_, G_, N_)                                                        \
   do {                                                                                    \
     using PC = PoolTmaCfg<D_, G_, N_>;                                                    \
@@ -117,10 +122,14 @@ void launch_frame_pool_tma(const FramePoolArgs& fa, int d, int smem, int grid, v
     pool_frames_tma_kernel<D_, G_, N_><<<grid, PC::THREADS, tsmem, S(stream)>>>(fa);      \
   } while (0)
   if (d == 128) {
-    if (pcfg == 1) LF_POOL_LAUNCH(128, 4, 4);
+    if (pcfg == 3) LF_POOL_LAUNCH(128, 8, 8);
+    else if (pcfg == 2) LF_POOL_LAUNCH(128, 4, 8);
+    else if (pcfg == 1) LF_POOL_LAUNCH(128, 4, 4);
     else LF_POOL_LAUNCH(128, 2, 4);
   } else {
-    if (pcfg == 1) LF_POOL_LAUNCH(64, 4, 4);
+    if (pcfg == 3) LF_POOL_LAUNCH(64, 8, 8);
+    else if (pcfg == 2) LF_POOL_LAUNCH(64, 4, 8);
+    else if (pcfg == 1) LF_POOL_LAUNCH(64, 4, 4);
     else LF_POOL_LAUNCH(64, 2, 4);
   }
 #undef LF_POOL_LAUNCH

@@ -60,7 +60,7 @@ def test_topk_indices(lf):
         assert got.tolist() == c["indices"], c
 
 
-@pytest.mark.parametrize("pool_cfg", ["2x4", "4x4"])
+@pytest.mark.parametrize("pool_cfg", ["2x4", "4x4", "4x8", "8x8"])
 @pytest.mark.parametrize("kind", ["aligned", "framewise"])
 def test_compress_bit_exact(lf, kind, pool_cfg, monkeypatch):
     # every (consumer groups x ring stages) variant of the TMA pooling kernel
