@@ -2,7 +2,11 @@
 
 Each backend exposes ``.name``, ``.layout``, ``.run(q, k, v, chunk_index)``,
 ``.stats_log`` and ``.mask_log`` (``HsaBackend`` also ``.plan``), so the
-reference's ``denoise_step``/``rollout`` can drive them unchanged.  All
+reference's ``denoise_step``/``rollout`` can drive them unchanged
+(tests/test_gpu_backends.py runs ``chunkattn.rollout`` with them).  ``layout``
+may be this package's ``ChunkLayout`` or the reference's: ``.layout`` keeps
+the caller's object, so ``rollout()``'s ``backend.layout == layout`` check
+(rollout.py:281-282) holds either way.  All
 attention work runs on the GPU; inputs/outputs keep the caller's container
 type (numpy in, numpy out).
 """
@@ -12,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from .attention import _Timer, block_sparse_attention, dense_attention
-from .layout import AttnStats, BlockMask, ChunkLayout, ceil_div
+from .layout import AttnStats, BlockMask, ChunkLayout, as_layout, ceil_div, is_aligned
 from .planner import SparsityPlan
 from .selection import SelectionConfig, hsa_attention
 
@@ -57,7 +61,7 @@ class HsaBackend:
         self.plan = plan
         self.cfg = cfg or SelectionConfig()
         self.threads = threads
-        self.framewise = (not layout.aligned) if framewise is None else framewise
+        self.framewise = (not is_aligned(layout)) if framewise is None else framewise
         self.stats_log: list[AttnStats] = []
         self.mask_log: list[BlockMask] = []
 

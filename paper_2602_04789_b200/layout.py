@@ -18,13 +18,29 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
-@dataclass(frozen=True)
+LAYOUT_FIELDS = ("f", "n", "b_q", "b_kv", "d", "N")
+
+
+def _layout_key(obj):
+    """(f, n, b_q, b_kv, d, N) of any layout-like object, else None."""
+    try:
+        return tuple(int(getattr(obj, name)) for name in LAYOUT_FIELDS)
+    except (AttributeError, TypeError, ValueError):
+        return None
+
+
+@dataclass(frozen=True, eq=False)
 class ChunkLayout:
     """Tiling geometry for a chunked rollout (attention.py:45-96).
 
     f frames per chunk, n tokens per frame, b_q x b_kv tiles, head dim d,
     N chunks.  Derived counts use ceilings (contiguous tiling); the framewise
     ragged extension uses ``framewise_*`` helpers instead.
+
+    Equality is by the six fields against ANY layout-like object, so the
+    reference's own ``chunkattn.ChunkLayout`` and this one compare equal when
+    they describe the same geometry: ``chunkattn.rollout`` checks
+    ``backend.layout == layout`` (rollout.py:281-282).
     """
 
     f: int
@@ -35,9 +51,22 @@ class ChunkLayout:
     N: int
 
     def __post_init__(self):
-        for name in ("f", "n", "b_q", "b_kv", "d", "N"):
+        for name in LAYOUT_FIELDS:
             if getattr(self, name) < 1:
                 raise ValueError(f"layout field {name} must be >= 1, got {getattr(self, name)}")
+
+    def __eq__(self, other):
+        key = _layout_key(other)
+        if key is None:
+            return NotImplemented
+        return key == _layout_key(self)
+
+    def __ne__(self, other):
+        eq = self.__eq__(other)
+        return eq if eq is NotImplemented else not eq
+
+    def __hash__(self):
+        return hash(_layout_key(self))
 
     @property
     def chunk_tokens(self) -> int:
@@ -69,7 +98,7 @@ class ChunkLayout:
     # --- framewise ragged extension: frame-local block tiling
     @property
     def aligned(self) -> bool:
-        return self.n % self.b_q == 0 and self.n % self.b_kv == 0
+        return is_aligned(self)
 
     @property
     def frame_q_blocks(self) -> int:
@@ -80,6 +109,22 @@ class ChunkLayout:
 
     def framewise_k_blocks(self, i: int) -> int:
         return self.total_blocks(i)
+
+
+def is_aligned(layout) -> bool:
+    """Frame-aligned tiling (the reference's selection precondition, selection.py:88-92);
+    works on any layout-like object, the reference's ChunkLayout included."""
+    return layout.n % layout.b_q == 0 and layout.n % layout.b_kv == 0
+
+
+def as_layout(layout) -> ChunkLayout:
+    """This package's ChunkLayout for any layout-like object (e.g. chunkattn.ChunkLayout)."""
+    if isinstance(layout, ChunkLayout):
+        return layout
+    key = _layout_key(layout)
+    if key is None:
+        raise TypeError(f"not a chunk layout: {layout!r}")
+    return ChunkLayout(*key)
 
 
 class BlockMask:

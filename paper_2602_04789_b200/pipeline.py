@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .layout import BlockMask, ChunkLayout
+from .layout import BlockMask, ChunkLayout, as_layout, is_aligned
 from .selection import SelectionConfig, mask_from_lists, tilings
 
 
@@ -24,12 +24,12 @@ class HsaPipeline:
     def __init__(self, layout: ChunkLayout, heads: int, chunk_index: int,
                  cfg: SelectionConfig | None = None, framewise: bool | None = None,
                  out_dtype=torch.bfloat16, device=None):
-        self.layout = layout
+        self.layout = layout = as_layout(layout)
         self.heads = int(heads)
         self.chunk = int(chunk_index)
         self.cfg = cfg or SelectionConfig()
-        self.framewise = (not layout.aligned) if framewise is None else bool(framewise)
-        if not self.framewise and not layout.aligned:
+        self.framewise = (not is_aligned(self.layout)) if framewise is None else bool(framewise)
+        if not self.framewise and not is_aligned(self.layout):
             raise ValueError(
                 f"selection needs b_q and b_kv to divide n: n={layout.n}, b_q={layout.b_q}, "
                 f"b_kv={layout.b_kv}")

@@ -25,7 +25,7 @@ import math
 import torch
 
 from . import device as D
-from .layout import ChunkLayout
+from .layout import ChunkLayout, as_layout, is_aligned
 from .planner import SparsityPlan
 from .selection import SelectionConfig, tilings
 
@@ -34,12 +34,12 @@ class HsaRollout:
     def __init__(self, layout: ChunkLayout, heads: int, plan: SparsityPlan | None = None,
                  cfg: SelectionConfig | None = None, framewise: bool | None = None,
                  out_dtype=torch.bfloat16, device=None):
-        self.layout = layout
+        self.layout = layout = as_layout(layout)
         self.heads = int(heads)
         self.plan = plan
         self.cfg = cfg or SelectionConfig()
-        self.framewise = (not layout.aligned) if framewise is None else bool(framewise)
-        if not self.framewise and not layout.aligned:
+        self.framewise = (not is_aligned(self.layout)) if framewise is None else bool(framewise)
+        if not self.framewise and not is_aligned(self.layout):
             raise ValueError(
                 f"selection needs b_q and b_kv to divide n: n={layout.n}, b_q={layout.b_q}, "
                 f"b_kv={layout.b_kv}")

@@ -25,7 +25,7 @@ import torch
 from . import _convert as C
 from . import device as D
 from .attention import _Timer, effective_flops
-from .layout import AttnStats, BlockMask, ChunkLayout
+from .layout import AttnStats, BlockMask, ChunkLayout, as_layout
 from .planner import chunk_block_budget
 
 _BUDGET_MODES = ("global", "per-frame")
@@ -98,6 +98,7 @@ def _dev_tensor(a):
 def compress(q, k, chunk_index: int, layout: ChunkLayout, *, framewise: bool = False
              ) -> CompressedViews:
     """Mean-pool q and k into block summaries plus past frame summaries (selection.py:95-114)."""
+    layout = as_layout(layout)
     if not framewise:
         _require_frame_aligned(layout)
     layout.check_chunk(chunk_index)
@@ -176,6 +177,7 @@ def select_blocks(views: CompressedViews, r: int, frames, budget: int,
 def build_mask(selections, chunk_index: int, layout: ChunkLayout, *, framewise: bool = False
                ) -> BlockMask:
     """Current chunk dense, past blocks as selected (selection.py:178-193)."""
+    layout = as_layout(layout)
     if not framewise:
         _require_frame_aligned(layout)
     n_q = layout.framewise_q_blocks() if framewise else layout.q_blocks
@@ -212,6 +214,7 @@ def hsa_attention(q, k, v, chunk_index: int, s_i: float, cfg: SelectionConfig,
     kernel.  fp32 inputs are pooled in fp32 (bit-exact selection) and cast to
     bf16 for the tensor-core attention.
     """
+    layout = as_layout(layout)
     if not 0.0 <= s_i < 1.0:
         raise ValueError(f"s_i must lie in [0, 1), got {s_i}")
     if not framewise:

@@ -140,3 +140,16 @@ def test_plan_json_round_trip():
     text = lf.plan_to_json(plan, lay)
     back, lay2 = lf.plan_from_json(text)
     assert lay2 == lay and back == plan and lf.plan_to_json(back, lay2) == text
+
+
+def test_reference_staged_for_gpu_box():
+    """oracle/make_ref.py copies the pure-Python reference into oracle/_ref (unmodified)."""
+    import filecmp
+    from oracle import make_ref
+    if not os.path.isdir(make_ref.SRC):
+        pytest.skip("no /root/reference here (GPU box): the staged copy travels instead")
+    d = make_ref.stage()
+    assert d and make_ref.ref_path() == d
+    names = sorted(x for x in os.listdir(make_ref.SRC) if x.endswith(".py"))
+    match, mismatch, errors = filecmp.cmpfiles(make_ref.SRC, make_ref.DST, names, shallow=False)
+    assert not mismatch and not errors and len(match) == len(names) == 8
