@@ -197,6 +197,21 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
                     float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
                     void* stream);
 
+/* Split-KV partials and schedule counters of one attention launch over `heads`
+ * heads of a `q_tiling` query axis with head dim d (worst case over both query-
+ * tile geometries and the current device's SM count).  The scratch passed to
+ * lf_attention_ws must be zero-filled once when allocated; every launch leaves
+ * its counters at zero again, so it is reusable (and graph-replayable), but by
+ * ONE launch in flight at a time.  lf_attention / lf_attention_ex use a
+ * library-owned scratch per device instead (one launch in flight per device). */
+size_t lf_attention_scratch_bytes(int32_t heads, lf_tiling q_tiling, int32_t d);
+int lf_attention_ws(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                    const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                    int32_t dense_lo, int32_t dense_hi, float scale, void* out,
+                    int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
+                    float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
+                    void* scratch, size_t scratch_bytes, void* stream);
+
 /* One full hot-path call for all heads of one layer at one denoising step of
  * chunk i: compress -> select -> plan tiles -> sparse attention.  Replaces
  * selection.py:196-231 (hsa_attention).  Workspace from lf_hsa_workspace_bytes. */
@@ -217,12 +232,36 @@ typedef struct {
   double s_i_host;          /* host copy of s_i for LF_KERNEL_AUTO (NaN: unknown) */
 } lf_hsa_args;
 
+/* The workspace holds every intermediate of the call (summaries, selections,
+ * tile plans) and the attention scratch (lf_attention_scratch_bytes): zero-fill
+ * it once when allocating it.  One call in flight per workspace. */
 size_t lf_hsa_workspace_bytes(const lf_hsa_args* a);
 /* Device pointers into the workspace (for reading selections back). */
 int lf_hsa_views(const lf_hsa_args* a, void* workspace, float** q_block, float** k_block,
                  float** k_frame, int32_t** blocks, int32_t** count, int32_t** frames,
                  int32_t** budget, int32_t* cap, int32_t* frame_cap);
 int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Library options: experiment and test knobs, read ONCE from the environment
+ * at first use (the variable named after each) and settable programmatically;
+ * nothing reads the environment on a launch path.  -1 = automatic. */
+#define LF_OPT_POOL_CFG 0     /* LF_POOL_CFG: pooling groups x stages, -1 auto, 0 2x4,
+                                 1 4x4, 2 4x8, 3 8x8 (all bit-identical)            */
+#define LF_OPT_POOL_NO_TMA 1  /* LF_POOL_NO_TMA: 1 = register-streaming pooling     */
+#define LF_OPT_ATTN_SPLIT 2   /* LF_ATTN_SPLIT: 1..4 = split EVERY attention item in
+                                 that many key ranges (test hook), 0/-1 = tail only  */
+#define LF_OPT_ATTN_SCHED 3   /* LF_ATTN_DYNAMIC=1 / LF_ATTN_STATIC=1: 1 dynamic, 0
+                                 round-robin, -1 auto (dynamic on block-aligned)    */
+#define LF_OPT_PLAN_WARP 4    /* LF_PLAN_WARP: 1 = warp-per-tile planner             */
+#define LF_OPT_SELECT_WARP 5  /* LF_SELECT_WARP: 1 = warp-per-query-block selection  */
+#define LF_OPT_ATTN_DEBUG 6   /* LF_ATTN_DEBUG: 1 skip softmax, 2 event trace        */
+#define LF_OPT_ATTN_POLY 7    /* LF_ATTN_POLY: polynomial exp2 on every n-th pair    */
+#define LF_OPT_ATTN_KERNEL 8  /* LF_ATTN_VER (5/7): forced attention kernel, 0 auto  */
+#define LF_OPT_QTILE 9        /* LF_QTILE (blocks|rows) / lf_set_qtile_mode           */
+#define LF_OPT_TRACE_CTA 10   /* LF_ATTN_TRACE_CTA                                   */
+#define LF_OPT_COUNT 11
+int lf_set_option(int32_t opt, int32_t value); /* LF_ERR_INVALID for an unknown opt */
+int lf_get_option(int32_t opt);                /* -2 for an unknown opt             */
 
 /* Helpers for the per-row drop-in functions. */
 /* out[r] = <A[r,:], x> in fp64 (compensated), A fp32 [rows][d].  frame_scores. */

@@ -8,6 +8,7 @@ compute entry point raises ``RuntimeError``.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -30,8 +31,16 @@ EXPORTS = (
     "lf_cag_plan", "lf_plan_tile_rows", "lf_pool_chunk_k", "lf_set_qtile_mode",
     "lf_qtile_mode", "lf_plan_tile_count", "lf_plan_tiles", "lf_attention", "lf_attention_ex",
     "lf_attention_kernel_choice", "lf_hsa_workspace_bytes", "lf_hsa_views",
-    "lf_hsa_forward", "lf_rowdot", "lf_topk",
+    "lf_hsa_forward", "lf_rowdot", "lf_topk", "lf_attention_ws", "lf_attention_scratch_bytes",
+    "lf_set_option", "lf_get_option",
 )
+
+# library options (include/lfattn.h LF_OPT_*)
+OPTIONS = {
+    "pool_cfg": 0, "pool_no_tma": 1, "attn_split": 2, "attn_sched": 3, "plan_warp": 4,
+    "select_warp": 5, "attn_debug": 6, "attn_poly": 7, "attn_kernel": 8, "qtile": 9,
+    "trace_cta": 10,
+}
 
 
 class LfTiling(ctypes.Structure):
@@ -84,6 +93,12 @@ _SIGS = {
     "lf_attention_ex": ([ctypes.POINTER(LfMat), ctypes.POINTER(LfMat), ctypes.POINTER(LfMat),
                          LfTiling, _P, _P, _I, _I, _I, ctypes.c_float, _P, _I, ctypes.c_int64,
                          ctypes.c_int64, _P, _P, _I, _I, _P], ctypes.c_int),
+    "lf_attention_ws": ([ctypes.POINTER(LfMat), ctypes.POINTER(LfMat), ctypes.POINTER(LfMat),
+                         LfTiling, _P, _P, _I, _I, _I, ctypes.c_float, _P, _I, ctypes.c_int64,
+                         ctypes.c_int64, _P, _P, _I, _I, _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "lf_attention_scratch_bytes": ([_I, LfTiling, _I], ctypes.c_size_t),
+    "lf_set_option": ([_I, _I], ctypes.c_int),
+    "lf_get_option": ([_I], ctypes.c_int),
     "lf_attention_kernel_choice": ([_I, _I, _I, _I], ctypes.c_int),
     "lf_hsa_workspace_bytes": ([ctypes.POINTER(LfHsaArgs)], ctypes.c_size_t),
     "lf_hsa_views": ([ctypes.POINTER(LfHsaArgs), _P] + [ctypes.POINTER(_P)] * 7 +
@@ -118,6 +133,26 @@ def lib():
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2602_04789_b200 needs a CUDA (sm_100a) device; none is visible")
     return load_library()
+
+
+def set_option(name: str, value: int) -> int:
+    """Set a library option (LF_OPT_*); returns the previous value."""
+    lb = load_library()
+    o = OPTIONS[name]
+    prev = int(lb.lf_get_option(o))
+    check(lb.lf_set_option(o, int(value)))
+    return prev
+
+
+@contextlib.contextmanager
+def option(name: str, value: int):
+    """Library option `name` = value inside the block (tests and experiments;
+    the library reads its environment knobs once, so setenv does not work)."""
+    prev = set_option(name, value)
+    try:
+        yield
+    finally:
+        set_option(name, prev)
 
 
 def check(status: int) -> None:

@@ -1,4 +1,4 @@
-// Shared pieces of the two tcgen05 attention kernels (attn_sm100_v3.cuh: one
+// Shared pieces of the tcgen05 attention kernels (attn_sm100_v7.cuh: one
 // query tile per CTA; attn_sm100_v5.cuh: query-tile pairs).
 //
 // Contract, restating block_sparse_attention / _stream_rows

@@ -3,11 +3,14 @@
 // planner.py:126-175 (allocate) with _solve_clamped 178-208, alpha_schedule
 // 56-66, ChunkLengths.weights 51-53, s_max_for_chunk 113-116 and
 // chunk_block_budget 119-123.  Every elementwise operation is the same IEEE
-// double operation the reference performs (sqrt, /, clip, floor(x+0.5)), and
-// the weights are exact integers, so alpha, s_max, clamps and budgets agree
-// bit for bit; the two inexact reductions (sum(alpha*w) via BLAS ddot and the
-// fixed-chunk spend) are compensated sums here, within the reference's own
-// 1e-12 relative tolerance (test_planner.py:136-144).
+// double operation the reference performs (sqrt, /, clip, floor(x+0.5)),
+// written with explicit __d*_rn intrinsics where a multiply meets an add so
+// that nvcc's default fma contraction cannot fuse them (NumPy rounds the
+// product and the sum separately); the weights are exact integers, so alpha,
+// s_max, clamps and budgets agree bit for bit.  The two inexact reductions
+// (sum(alpha*w) via BLAS ddot and the fixed-chunk spend) are compensated sums
+// here, within the reference's own 1e-12 relative tolerance
+// (test_planner.py:136-144): BLAS's summation order is not reproducible.
 #pragma once
 #include "common.cuh"
 
@@ -55,7 +58,7 @@ __global__ void cag_kernel(CagArgs a) {
   double beta = 0.0;
   *a.status = LF_OK;
   if (any_planned) {
-    const double target = (1.0 - a.s_target) * w_planned;
+    const double target = __dmul_rn(__dsub_rn(1.0, a.s_target), w_planned);
     // free set as bit flags in s-space: use clamped[] for "clamped so far";
     // free = planned && !frozen
     unsigned char frozen[1024];
@@ -66,10 +69,10 @@ __global__ void cag_kernel(CagArgs a) {
       for (int i = 0; i < N; ++i) {
         if (!planned(i)) continue;
         if (!frozen[i]) {
-          dd_add(den, a.alpha[i] * w_of(i));
+          dd_add(den, __dmul_rn(a.alpha[i], w_of(i)));
           wfree += w_of(i);
         } else {
-          dd_add(fixed, (1.0 - a.s[i]) * w_of(i));
+          dd_add(fixed, __dmul_rn(__dsub_rn(1.0, a.s[i]), w_of(i)));
         }
       }
       double dn = dd_value(den);
@@ -78,13 +81,13 @@ __global__ void cag_kernel(CagArgs a) {
         return;
       }
       double resid = target - dd_value(fixed);
-      beta = (resid - (1.0 - a.s_base) * wfree) / dn;
+      beta = __ddiv_rn(__dsub_rn(resid, __dmul_rn(__dsub_rn(1.0, a.s_base), wfree)), dn);
       bool any_new = false, any_left = false;
       unsigned char newly[1024];
       for (int i = 0; i < N; ++i) {
         newly[i] = 0;
         if (!planned(i) || frozen[i]) continue;
-        double raw = a.s_base - a.alpha[i] * beta;
+        double raw = __dsub_rn(a.s_base, __dmul_rn(a.alpha[i], beta));
         double v = raw > 0.0 ? raw : 0.0;       // np.clip -> minimum(maximum(raw, 0), hi)
         double hi = shi_of(i);
         v = v < hi ? v : hi;
@@ -110,8 +113,8 @@ __global__ void cag_kernel(CagArgs a) {
   DD spend{0.0, 0.0};
   for (int i = 0; i < N; ++i) {
     long long total = (long long)(i + 1) * cur;
-    a.budgets[i] = (int)floor((1.0 - a.s[i]) * (double)total + 0.5);
-    if (planned(i)) dd_add(spend, (1.0 - a.s[i]) * w_of(i));
+    a.budgets[i] = budget_round(a.s[i], total);
+    if (planned(i)) dd_add(spend, __dmul_rn(__dsub_rn(1.0, a.s[i]), w_of(i)));
   }
   a.scalars[0] = beta;
   a.scalars[1] = any_planned ? dd_value(spend) / w_planned : 1.0;

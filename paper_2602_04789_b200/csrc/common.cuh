@@ -70,14 +70,23 @@ __host__ __device__ inline void qtile_rows(const Tiling& qt, int mode, int t, in
 struct DD {
   double hi, lo;
 };
+// TwoSum accumulation.  Explicit round-to-nearest intrinsics: nvcc's default
+// --fmad=true may otherwise contract a caller's product b = x*y into the first
+// add (a.hi + x*y -> fma), which breaks the error-free transformation.
 __device__ __forceinline__ void dd_add(DD& a, double b) {
-  double s = a.hi + b;
-  double bb = s - a.hi;
-  double err = (a.hi - (s - bb)) + (b - bb);
+  const double s = __dadd_rn(a.hi, b);
+  const double bb = __dsub_rn(s, a.hi);
+  const double err = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, bb)), __dsub_rn(b, bb));
   a.hi = s;
-  a.lo += err;
+  a.lo = __dadd_rn(a.lo, err);
 }
-__device__ __forceinline__ double dd_value(const DD& a) { return a.hi + a.lo; }
+__device__ __forceinline__ double dd_value(const DD& a) { return __dadd_rn(a.hi, a.lo); }
+
+// round_half_up((1 - s) * total) (planner.py:28-29, 119-123) with NumPy's two
+// roundings (product, then + 0.5): never contracted into an fma
+__device__ __forceinline__ int budget_round(double s, long long total) {
+  return (int)floor(__dadd_rn(__dmul_rn(__dsub_rn(1.0, s), (double)total), 0.5));
+}
 
 // ---------------------------------------------------------------------------
 // PTX: shared-memory addresses, mbarriers, fences

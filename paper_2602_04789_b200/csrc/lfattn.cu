@@ -6,7 +6,8 @@
 #include <cstring>
 #include <mutex>
 
-#include "attn_sm100_v3.cuh"
+#include <atomic>
+
 #include "attn_sm100_v5.cuh"
 #include "attn_sm100_v7.cuh"
 #include "cag.cuh"
@@ -102,17 +103,73 @@ int check_tiling(lf_tiling t, const char* name) {
   return LF_OK;
 }
 
+// ---- library options (include/lfattn.h LF_OPT_*): the environment is read once,
+// at first use; launch paths read the cached values only
+std::atomic<int> g_opt[LF_OPT_COUNT];
+int g_env_qtile = -1;  // LF_QTILE from the environment (lf_set_qtile_mode(-1) falls back to it)
+std::once_flag g_opt_once;
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+void init_options() {
+  std::call_once(g_opt_once, [] {
+    for (int i = 0; i < LF_OPT_COUNT; ++i) g_opt[i].store(-1);
+    if (const char* pc = getenv("LF_POOL_CFG")) {
+      const int v = !strcmp(pc, "2x4") ? 0 : !strcmp(pc, "4x4") ? 1 : !strcmp(pc, "4x8") ? 2
+                  : !strcmp(pc, "8x8") ? 3 : -1;
+      if (v < 0) fprintf(stderr, "lfattn: ignoring unknown LF_POOL_CFG=%s (2x4|4x4|4x8|8x8)\n", pc);
+      g_opt[LF_OPT_POOL_CFG].store(v);
+    }
+    g_opt[LF_OPT_POOL_NO_TMA].store(getenv("LF_POOL_NO_TMA") ? 1 : 0);
+    g_opt[LF_OPT_ATTN_SPLIT].store(env_int("LF_ATTN_SPLIT", 0));
+    g_opt[LF_OPT_ATTN_SCHED].store(getenv("LF_ATTN_DYNAMIC") ? 1 : getenv("LF_ATTN_STATIC") ? 0 : -1);
+    g_opt[LF_OPT_PLAN_WARP].store(getenv("LF_PLAN_WARP") ? 1 : 0);
+    g_opt[LF_OPT_SELECT_WARP].store(getenv("LF_SELECT_WARP") ? 1 : 0);
+    g_opt[LF_OPT_ATTN_DEBUG].store(env_int("LF_ATTN_DEBUG", 0));
+    g_opt[LF_OPT_ATTN_POLY].store(env_int("LF_ATTN_POLY", 0));
+    const int ver = env_int("LF_ATTN_VER", 0);
+    g_opt[LF_OPT_ATTN_KERNEL].store(ver == 5 ? LF_KERNEL_PAIR : ver == 7 ? LF_KERNEL_TILE : 0);
+    if (const char* e = getenv("LF_QTILE")) g_env_qtile = !strcmp(e, "blocks") ? 1 : *e ? 0 : -1;
+    g_opt[LF_OPT_QTILE].store(-1);
+    g_opt[LF_OPT_TRACE_CTA].store(env_int("LF_ATTN_TRACE_CTA", 0));
+  });
+}
+
+int opt(int i) {
+  init_options();
+  return g_opt[i].load(std::memory_order_relaxed);
+}
+
+// SM count of the current device (cached per device ordinal)
+int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  if (dev < 0 || dev >= 64) dev = 0;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+    cudaGetLastError();
+    v = 148;
+  }
+  cache[dev].store(v, std::memory_order_relaxed);
+  return v;
+}
+
 // K1 launch (pool.cuh pool_frames_tma_kernel): contiguous bf16 rows, d 64/128,
-// blocks <= 64 rows. LF_POOL_CFG picks (consumer groups x ring stages):
-// "4x4" (default) or "2x4".
+// blocks <= 64 rows.  LF_OPT_POOL_CFG picks (consumer groups x ring stages).
 void launch_frame_pool_tma(const FramePoolArgs& fa, int d, int smem, int grid, void* stream) {
-  const char* pc = getenv("LF_POOL_CFG");
-  int pcfg = !pc ? LF_POOL_DEFAULT : !strcmp(pc, "4x4") ? 1 : !strcmp(pc, "4x8") ? 2 : 0;
-  // fewer CTAs than SMs (a single chunk commit: H*f CTAs): one CTA per SM and
-  // the frame's blocks are the critical path, so 8 consumer groups (8 blocks
-  // summed at once) over an 8-stage ring
-  if (!pc && grid < 148) pcfg = 3;
-  if (pc && !strcmp(pc, "8x8")) pcfg = 3;
+  int pcfg = opt(LF_OPT_POOL_CFG);
+  // automatic: 4 groups x 4 stages; with fewer CTAs than SMs (a single chunk
+  // commit: H*f CTAs) one CTA per SM and the frame's blocks are the critical
+  // path, so 8 consumer groups (8 blocks summed at once) over an 8-stage ring
+  if (pcfg < 0) pcfg = grid < sm_count() ? 3 : LF_POOL_DEFAULT;
 #define LF_POOL_LAUNCH(D_, G_, N_)                                                        \
   do {                                                                                    \
     using PC = PoolTmaCfg<D_, G_, N_>;                                                    \
@@ -194,18 +251,17 @@ int launch_pool(PoolArgs& a, int dtype, int vec, int ns, cudaStream_t st) {
                           : launch_pool_t<float>(a, vec, ns, st);
 }
 
-// forced attention kernel (LF_ATTN_VER=3|5, for experiments), 0 = per call
-int attn_ver() {
-  static const int v = getenv("LF_ATTN_VER") ? atoi(getenv("LF_ATTN_VER")) : 0;
-  return v == 3 || v == 5 || v == 7 ? v : 0;
+// forced attention kernel (LF_OPT_ATTN_KERNEL, for experiments), 0 = per call
+int forced_kernel() {
+  const int v = opt(LF_OPT_ATTN_KERNEL);
+  return v == LF_KERNEL_PAIR || v == LF_KERNEL_TILE ? v : 0;
 }
 
 // Kernel choice.  The tile kernel with two softmax sets (v7) matches or beats
 // the pair kernel (v5) at every measured shape (B200: c2 1025 vs 907 TFLOP/s,
 // c3 576 vs 549, c5_s50 524 vs 480, c4 1041 vs 1043, c5_dense 1051 vs 1047)
 // without stream-K merges, so LF_KERNEL_AUTO takes it; the pair kernel stays
-// available explicitly (LF_KERNEL_PAIR).  LF_ATTN_VER=3 selects the previous
-// single-softmax tile kernel for comparisons.
+// available explicitly (LF_KERNEL_PAIR).
 int choose_kernel(int heads, int n_qtiles, int dense_keys, int past_tiles, int sms) {
   (void)heads; (void)n_qtiles; (void)dense_keys; (void)past_tiles; (void)sms;
   return LF_KERNEL_TILE;
@@ -230,15 +286,11 @@ int max_qblocks_per_tile(lf_tiling qt, int rows = kTileRows) {
 // block-aligned tiles (two query blocks each) when requested (lf_set_qtile_mode,
 // else LF_QTILE=blocks) and the blocks are 33..64 rows, else 0 = 128-row tiles.
 // The tile planner and the attention kernel must agree: both read it here.
-int g_qmode_req = -1;                 // lf_set_qtile_mode
 thread_local int g_qmode_scope = -1;  // automatic choice of the lf_hsa_* call in progress
 constexpr int kBlockTilesMinPast = 16;
 int qmode_for(lf_tiling qt) {
-  int req = g_qmode_req;
-  if (req < 0) {
-    const char* e = getenv("LF_QTILE");
-    if (e && *e) req = !strcmp(e, "blocks") ? 1 : 0;
-  }
+  int req = opt(LF_OPT_QTILE);  // lf_set_qtile_mode
+  if (req < 0) req = g_env_qtile;
   if (req < 0) req = g_qmode_scope > 0 ? 1 : 0;
   return req && qt.block > 32 && qt.block <= 64 ? 1 : 0;
 }
@@ -283,37 +335,85 @@ int seg_cap_for(int mq, int cap_blocks, int list_blocks, int b_kv) {
   return sc > 0 ? (int)sc : 1;
 }
 
-// Split-KV scratch (partials + merge counters), grown outside graph capture and
-// never freed: captured CUDA graphs may still point at an older buffer.
-// Layout [counters][part_ml][part_o]; counters stay zero between launches.
-bool split_scratch(size_t need_c, size_t need_ml, size_t need_o, cudaStream_t st, int** counters,
+// ---- attention scratch: [counters][part_ml][part_o]
+// counters = the dynamic schedule (8 ints) + one merge counter per split item;
+// the counter region has a FIXED size so it stays where it is (and zero)
+// whatever the partial regions of later launches need.  Kernels leave every
+// counter they touched at zero, so a zero-filled scratch stays valid.
+constexpr size_t kScratchCounters = 8192;  // ints
+constexpr size_t kScratchCounterBytes = kScratchCounters * 4;
+
+struct Scratch {
+  char* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+// the three regions of a launch in a scratch, false if it does not fit
+bool carve_scratch(Scratch s, size_t need_c, size_t need_ml, size_t need_o, int** counters,
                    float2** part_ml, float** part_o) {
-  static void* ws = nullptr;
-  static size_t cap_c = 0, cap_ml = 0, cap_o = 0;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  if (need_c > cap_c || need_ml > cap_ml || need_o > cap_o) {
+  if (!s.ptr || need_c > kScratchCounterBytes ||
+      kScratchCounterBytes + align_up(need_ml, 256) + need_o > s.bytes)
+    return false;
+  *counters = reinterpret_cast<int*>(s.ptr);
+  *part_ml = reinterpret_cast<float2*>(s.ptr + kScratchCounterBytes);
+  *part_o = reinterpret_cast<float*>(s.ptr + kScratchCounterBytes + align_up(need_ml, 256));
+  return true;
+}
+
+// Library-owned scratch of lf_attention / lf_attention_ex, one per device
+// ordinal, grown outside graph capture and never freed (captured graphs may
+// still point at an older buffer).
+struct DevScratch {
+  std::mutex mu;
+  Scratch s;
+};
+DevScratch g_dev_scratch[64];
+
+bool device_scratch(size_t need_c, size_t need_ml, size_t need_o, cudaStream_t st, Scratch* out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return false;
+  }
+  DevScratch& ds = g_dev_scratch[dev];
+  std::lock_guard<std::mutex> lock(ds.mu);
+  const size_t need = kScratchCounterBytes + align_up(need_ml, 256) + need_o;
+  if (need_c > kScratchCounterBytes) return false;
+  if (need > ds.s.bytes) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     if (cs != cudaStreamCaptureStatusNone) return false;
-    const size_t nc = need_c > cap_c ? need_c : cap_c, nm = need_ml > cap_ml ? need_ml : cap_ml,
-                 no = need_o > cap_o ? need_o : cap_o;
+    const size_t grown = need > 2 * ds.s.bytes ? need : 2 * ds.s.bytes;
     void* fresh = nullptr;
-    if (cudaMalloc(&fresh, nc + nm + no) != cudaSuccess) {
+    if (cudaMalloc(&fresh, grown) != cudaSuccess) {
       cudaGetLastError();
       return false;
     }
-    cudaMemsetAsync(fresh, 0, nc, st);
-    ws = fresh;
-    cap_c = nc;
-    cap_ml = nm;
-    cap_o = no;
+    cudaMemsetAsync(fresh, 0, kScratchCounterBytes, st);
+    ds.s.ptr = static_cast<char*>(fresh);
+    ds.s.bytes = grown;
   }
-  char* b = static_cast<char*>(ws);
-  *counters = reinterpret_cast<int*>(b);
-  *part_ml = reinterpret_cast<float2*>(b + cap_c);
-  *part_o = reinterpret_cast<float*>(b + cap_c + cap_ml);
+  *out = ds.s;
   return true;
+}
+
+// Scratch for one launch: the caller's (lf_attention_ws / lf_hsa_forward) if
+// given, else the device's library scratch.
+bool launch_scratch(const Scratch* caller, size_t need_c, size_t need_ml, size_t need_o,
+                    cudaStream_t st, int** counters, float2** part_ml, float** part_o) {
+  if (caller && carve_scratch(*caller, need_c, need_ml, need_o, counters, part_ml, part_o))
+    return true;
+  // no caller scratch, or one sized for the automatic split only (the
+  // LF_OPT_ATTN_SPLIT test hook splits every item): the device's scratch
+  Scratch s;
+  if (!device_scratch(need_c, need_ml, need_o, st, &s)) return false;
+  return carve_scratch(s, need_c, need_ml, need_o, counters, part_ml, part_o);
+}
+
+// worst case of the tile kernel (launch_tile) without the LF_OPT_ATTN_SPLIT hook:
+// <= sms split parts, 128 rows each
+size_t tile_scratch_bytes(int d, int sms) {
+  return kScratchCounterBytes + align_up((size_t)sms * 128 * 8, 256) + (size_t)sms * 128 * d * 4;
 }
 
 // v5: query-tile pairs; whole items round-robin, the tail (< grid items) stream-K
@@ -321,8 +421,8 @@ bool split_scratch(size_t need_c, size_t need_ml, size_t need_o, cudaStream_t st
 // clock64 event trace of CTA LF_ATTN_TRACE_CTA (kernels built with the trace macro)
 // and writes it to gpurun_out/attn_trace.txt after the fourth launch
 void setup_trace(AttnParams& p, void* stream) {
-  p.debug = getenv("LF_ATTN_DEBUG") ? atoi(getenv("LF_ATTN_DEBUG")) : 0;
-  if (p.debug == 2 && getenv("LF_ATTN_TRACE_CTA")) p.debug |= atoi(getenv("LF_ATTN_TRACE_CTA")) << 8;
+  p.debug = opt(LF_OPT_ATTN_DEBUG) > 0 ? opt(LF_OPT_ATTN_DEBUG) : 0;
+  if (p.debug == 2) p.debug |= (opt(LF_OPT_TRACE_CTA) > 0 ? opt(LF_OPT_TRACE_CTA) : 0) << 8;
   if ((p.debug & 255) == 2) {
     static long long* tr = nullptr;
     if (!tr) {
@@ -344,7 +444,7 @@ void setup_trace(AttnParams& p, void* stream) {
   }
 }
 
-int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
+int launch_v5(AttnParams& p, int heads, int d, int sms, const Scratch* scratch, void* stream) {
   const int n_pairs = (p.n_qtiles + 1) / 2;
   const int items = n_pairs * heads;
   const int G = sms < AttnCfg5<128>::MAX_TAIL ? sms : AttnCfg5<128>::MAX_TAIL;
@@ -358,7 +458,8 @@ int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
     const size_t need_c = align_up((size_t)G * 4, 256);
     const size_t need_ml = align_up((size_t)2 * G * 256 * 8, 256);
     const size_t need_o = (size_t)2 * G * 256 * d * 4;
-    if (!split_scratch(need_c, need_ml, need_o, S(stream), &p.counters, &p.part_ml, &p.part_o)) {
+    if (!launch_scratch(scratch, need_c, need_ml, need_o, S(stream), &p.counters, &p.part_ml,
+                        &p.part_o)) {
       p.counters = nullptr;
       p.part_ml = nullptr;
       p.part_o = nullptr;  // kernel falls back to whole tail items
@@ -367,7 +468,7 @@ int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
   const int grid = items < G && !p.part_o ? items : G;
   if (grid <= 0) return LF_OK;
   setup_trace(p, stream);
-  static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
+  const int poly = opt(LF_OPT_ATTN_POLY) > 0 ? opt(LF_OPT_ATTN_POLY) : 0;
 #define LF_V5(DD, PV)                                                                            \
   if (d == DD && poly == PV) {                                                                \
     cudaFuncSetAttribute(attn_fwd_v5_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -380,36 +481,40 @@ int launch_v5(AttnParams& p, int heads, int d, int sms, void* stream) {
   return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v5: d=%d poly=%d not instantiated", d, poly);
 }
 
-// v3 (legacy): one query tile per CTA, split-KV of the last partial round
-int launch_v3(AttnParams& p, int heads, int d, int sms, void* stream) {
+// tile kernel (v7): one query tile per CTA, split-KV of the last partial round
+int launch_tile(AttnParams& p, int heads, int d, int sms, const Scratch* scratch, void* stream) {
   const int items = p.n_qtiles * heads;
   const int slots = sms;
   int rem = items >= slots ? items % slots : items;
   int tail_split = rem ? slots / rem : 1;
   tail_split = tail_split > 4 ? 4 : tail_split;
-  if (const char* e = getenv("LF_ATTN_SPLIT")) {  // test hook: split every item
-    tail_split = atoi(e);
-    tail_split = tail_split < 1 ? 1 : (tail_split > 4 ? 4 : tail_split);
+  if (opt(LF_OPT_ATTN_SPLIT) > 0) {  // test hook: split every item
+    tail_split = opt(LF_OPT_ATTN_SPLIT);
+    tail_split = tail_split > 4 ? 4 : tail_split;
     rem = items;
   }
   if (tail_split < 2) { rem = 0; tail_split = 1; }
-  // counters region: [8 ints: the dynamic schedule][rem tail counters]
-  // dynamic schedule for sparse plans (block-aligned geometry), where items
-  // differ in key-tile count: attention -2 % at c3, -4 % at c5_s70; static
-  // round-robin for dense-like plans (+2 % slower dynamic at c5_dense).
-  // LF_ATTN_STATIC=1 / LF_ATTN_DYNAMIC=1 force one (profiles/r01/sched_ab.txt).
-  const bool dyn = getenv("LF_ATTN_DYNAMIC") ? true : getenv("LF_ATTN_STATIC") ? false : p.qmode == 1;
+  // counters: [8 ints: the dynamic schedule][rem tail counters].  Dynamic
+  // schedule for sparse plans (block-aligned geometry), where items differ in
+  // key-tile count: attention -2 % at c3, -4 % at c5_s70; static round-robin
+  // for dense-like plans (+2 % slower dynamic at c5_dense).  LF_OPT_ATTN_SCHED
+  // forces one (profiles/r01/sched_ab.txt).
+  const int sched = opt(LF_OPT_ATTN_SCHED);
+  const bool dyn = sched >= 0 ? sched == 1 : p.qmode == 1;
   {
     const int nr = rem > 0 ? rem : 0;
-    const size_t need_c = align_up((size_t)(nr + 8) * 4, 256);
-    const size_t need_ml = align_up((size_t)nr * tail_split * 128 * 8, 256);
+    const size_t need_c = (size_t)(nr + 8) * 4;
+    const size_t need_ml = (size_t)nr * tail_split * 128 * 8;
     const size_t need_o = (size_t)nr * tail_split * 128 * d * 4;
     int* base = nullptr;
-    if (split_scratch(need_c, need_ml, need_o, S(stream), &base, &p.part_ml, &p.part_o)) {
+    if (launch_scratch(scratch, need_c, need_ml, need_o, S(stream), &base, &p.part_ml, &p.part_o)) {
       p.sched = dyn ? base : nullptr;
       p.counters = base + 8;
     } else {
       p.sched = nullptr;
+      p.counters = nullptr;
+      p.part_ml = nullptr;
+      p.part_o = nullptr;
       rem = 0;
       tail_split = 1;
     }
@@ -419,8 +524,7 @@ int launch_v3(AttnParams& p, int heads, int d, int sms, void* stream) {
   setup_trace(p, stream);
   const int work = p.full_items + rem * tail_split;
   const int grid = work < slots ? work : slots;
-  static const int poly = getenv("LF_ATTN_POLY") ? atoi(getenv("LF_ATTN_POLY")) : 0;
-  if (attn_ver() != 3) {
+  const int poly = opt(LF_OPT_ATTN_POLY) > 0 ? opt(LF_OPT_ATTN_POLY) : 0;
 #define LF_V7(DD, PV)                                                                         \
   if (d == DD && poly == PV) {                                                                \
     cudaFuncSetAttribute(attn_fwd_v7_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -428,20 +532,9 @@ int launch_v3(AttnParams& p, int heads, int d, int sms, void* stream) {
     attn_fwd_v7_kernel<DD, PV><<<grid, 320, AttnCfg7<DD>::SMEM, S(stream)>>>(p, work);        \
     return check_launch("attn_fwd_v7_kernel");                                               \
   }
-    LF_V7(128, 0) LF_V7(64, 0) LF_V7(128, 4)
+  LF_V7(128, 0) LF_V7(64, 0) LF_V7(128, 4)
 #undef LF_V7
-    return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v7: d=%d poly=%d not instantiated", d, poly);
-  }
-#define LF_V3(DD, PV)                                                                         \
-  if (d == DD && poly == PV) {                                                                \
-    cudaFuncSetAttribute(attn_fwd_v3_kernel<DD, 2, PV>,                                       \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg3<DD>::SMEM);    \
-    attn_fwd_v3_kernel<DD, 2, PV><<<grid, 320, AttnCfg3<DD>::SMEM, S(stream)>>>(p, work);     \
-    return check_launch("attn_fwd_v3_kernel");                                               \
-  }
-  LF_V3(128, 0) LF_V3(64, 0)
-#undef LF_V3
-  return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v3: d=%d poly=%d not instantiated", d, poly);
+  return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v7: d=%d poly=%d not instantiated", d, poly);
 }
 
 struct HsaGeom {
@@ -503,6 +596,8 @@ struct HsaWs {
   float *q_block, *k_block, *k_frame;
   int *blocks, *count, *frames, *budget, *seg_count;
   int4* segs;
+  char* scratch;  // attention split-KV scratch (zero-filled with the workspace)
+  size_t scratch_bytes;
   size_t bytes;
 };
 
@@ -523,6 +618,8 @@ HsaWs carve(const HsaGeom& g, void* base) {
   w.budget = reinterpret_cast<int*>(take(16));
   w.segs = reinterpret_cast<int4*>(take((size_t)g.H * g.ntiles * g.seg_cap * 16));
   w.seg_count = reinterpret_cast<int*>(take((size_t)g.H * g.ntiles * 4));
+  w.scratch_bytes = tile_scratch_bytes(g.d, sm_count());
+  w.scratch = take(w.scratch_bytes);
   w.bytes = off;
   return w;
 }
@@ -535,20 +632,29 @@ extern "C" {
 int lf_version(void) { return 100; }
 
 int lf_plan_tile_rows(void) { return plan_rows(); }
-void lf_set_qtile_mode(int32_t mode) { g_qmode_req = mode < 0 ? -1 : mode ? 1 : 0; }
+void lf_set_qtile_mode(int32_t mode) {
+  init_options();
+  g_opt[LF_OPT_QTILE].store(mode < 0 ? -1 : mode ? 1 : 0);
+}
+
+int lf_set_option(int32_t o, int32_t value) {
+  if (o < 0 || o >= LF_OPT_COUNT) return fail(LF_ERR_INVALID, "unknown option %d", o);
+  init_options();
+  g_opt[o].store(value);
+  return LF_OK;
+}
+
+int lf_get_option(int32_t o) {
+  if (o < 0 || o >= LF_OPT_COUNT) return -2;
+  return opt(o);
+}
 int lf_qtile_mode(lf_tiling q_tiling) { return qmode_for(q_tiling); }
 int lf_plan_tile_count(lf_tiling q_tiling) { return plan_tile_count(q_tiling); }
 
 int lf_attention_kernel_choice(int32_t heads, int32_t q_rows, int32_t dense_keys,
                                int32_t past_tiles_hint) {
-  if (attn_ver()) return attn_ver() == 5 ? LF_KERNEL_PAIR : LF_KERNEL_TILE;
-  int sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
-    cudaGetLastError();
-    sms = 148;
-  }
-  return choose_kernel(heads, (q_rows + 127) / 128, dense_keys, past_tiles_hint, sms);
+  if (forced_kernel()) return forced_kernel();
+  return choose_kernel(heads, (q_rows + 127) / 128, dense_keys, past_tiles_hint, sm_count());
 }
 
 const char* lf_strerror(int status) {
@@ -620,7 +726,7 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
       const int grid = q->heads * (fa.q_frames + fa.k_frames);
       // contiguous rows: TMA-staged variant (bulk copies of whole blocks)
       if ((d == 128 || d == 64) && q->row_stride == d && k->row_stride == d && q_tiling.block <= 64 &&
-          !getenv("LF_POOL_NO_TMA")) {
+          opt(LF_OPT_POOL_NO_TMA) != 1) {
         launch_frame_pool_tma(fa, d, smem, grid, stream);
         return check_launch("pool_frames_tma_kernel");
       }
@@ -680,6 +786,14 @@ int lf_pool_chunk_k(const lf_mat* k, lf_tiling k_tiling, int32_t blocks_per_fram
       (size_t)per * d * 4 > 96 * 1024)
     return fail(LF_ERR_UNSUPPORTED, "lf_pool_chunk_k: needs contiguous bf16 rows, d 64/128, "
                                     "whole frames, blocks <= 64 rows");
+  // outputs: the kernel stores float2 pairs per head at these strides
+  const long long frames = k_tiling.total / k_tiling.period;
+  if (kb_head_stride < frames * per * d || kf_head_stride < frames * d || (kb_head_stride & 1) ||
+      (kf_head_stride & 1) || reinterpret_cast<uintptr_t>(k_block) % 8 ||
+      reinterpret_cast<uintptr_t>(k_frame) % 8)
+    return fail(LF_ERR_INVALID, "lf_pool_chunk_k: output head strides (%lld, %lld) must be even "
+                "and >= (%lld, %lld), outputs 8-byte aligned", (long long)kb_head_stride,
+                (long long)kf_head_stride, frames * per * d, frames * d);
   FramePoolArgs fa;
   memset(&fa, 0, sizeof(fa));
   fa.k = static_cast<const __nv_bfloat16*>(k->ptr);
@@ -729,7 +843,7 @@ int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_hea
             max_cand, (long long)kb_head_stride, (long long)kf_head_stride};
   // one 4-warp CTA per (head, query block); its working set adds the flags
   const int cta_smem = spw + (int)align_up((size_t)(P > max_cand ? P : max_cand), 16);
-  if (!getenv("LF_SELECT_WARP") && cta_smem <= 200 * 1024) {
+  if (opt(LF_OPT_SELECT_WARP) != 1 && cta_smem <= 200 * 1024) {
     if (cta_smem > 48 * 1024)
       cudaFuncSetAttribute(select_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cta_smem);
     select_cta_kernel<<<heads * nqb, 128, cta_smem, S(stream)>>>(a);
@@ -794,7 +908,7 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
   wpc = wpc > 4 ? 4 : wpc;
   PlanArgs a{blocks, count, heads, nqb, cap, Tiling(q_tiling), Tiling(k_tiling), list_blocks,
              ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc, rows, qmode};
-  if (qmode || !getenv("LF_PLAN_WARP")) {  // the warp planner knows 128/256-row tiles only
+  if (qmode || opt(LF_OPT_PLAN_WARP) != 1) {  // the warp planner knows 128/256-row tiles only
     if (spw > 48 * 1024)
       cudaFuncSetAttribute(plan_tiles_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, spw);
     plan_tiles_cta_kernel<<<heads * ntiles, 128, spw, S(stream)>>>(a);
@@ -824,6 +938,23 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
                     int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
                     float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
                     void* stream) {
+  return lf_attention_ws(q, k, v, q_tiling, segs, seg_count, seg_cap, dense_lo, dense_hi, scale,
+                         out, out_dtype, out_row_stride, out_head_stride, lse, err_flag, kernel,
+                         past_tiles_hint, nullptr, 0, stream);
+}
+
+size_t lf_attention_scratch_bytes(int32_t heads, lf_tiling q_tiling, int32_t d) {
+  (void)heads;
+  (void)q_tiling;
+  return tile_scratch_bytes(d > 0 ? d : 128, sm_count());
+}
+
+int lf_attention_ws(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                    const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                    int32_t dense_lo, int32_t dense_hi, float scale, void* out,
+                    int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
+                    float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
+                    void* scratch, size_t scratch_bytes, void* stream) {
   int rc;
   if ((rc = check_mat(q, "q")) || (rc = check_mat(k, "k")) || (rc = check_mat(v, "v"))) return rc;
   if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
@@ -863,25 +994,23 @@ int lf_attention_ex(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
   p.out_head_stride = out_head_stride;
   p.lse = lse;
   p.err = err_flag;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = sm_count();
+  Scratch caller;
+  caller.ptr = static_cast<char*>(scratch);
+  caller.bytes = scratch_bytes;
+  const Scratch* cs = scratch ? &caller : nullptr;
   p.plan_pairs = plan_rows() != kTileRows;
   if (kernel != LF_KERNEL_TILE && kernel != LF_KERNEL_PAIR)
     kernel = choose_kernel(q->heads, p.n_qtiles, dense_hi > dense_lo ? dense_hi - dense_lo : 0,
                            past_tiles_hint, sms);
-  if (attn_ver()) kernel = attn_ver() == 5 ? LF_KERNEL_PAIR : LF_KERNEL_TILE;
+  if (forced_kernel()) kernel = forced_kernel();
   if (p.qmode) kernel = LF_KERNEL_TILE;  // the pair kernel has 128-row tiles only
   if (kernel == LF_KERNEL_PAIR) {
-    p.tma_out = out_dtype == LF_BF16 && !getenv("LF_ATTN_NO_TMA_OUT") &&
+    p.tma_out = out_dtype == LF_BF16 &&
                 make_out_map(&p.to, out, q->d, q->rows, q->heads, out_row_stride, out_head_stride);
-    return launch_v5(p, q->heads, q->d, sms, stream);
+    return launch_v5(p, q->heads, q->d, sms, cs, stream);
   }
-  return launch_v3(p, q->heads, q->d, sms, stream);
+  return launch_tile(p, q->heads, q->d, sms, cs, stream);
 }
 
 size_t lf_hsa_workspace_bytes(const lf_hsa_args* a) {
@@ -936,11 +1065,11 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
     return rc;
   lf_mat kk = a->k, vv = a->v;
   kk.rows = vv.rows = a->chunk_index * a->f * a->n;
-  return lf_attention_ex(&a->q, &kk, &vv, g.qt, reinterpret_cast<const int32_t*>(w.segs),
+  return lf_attention_ws(&a->q, &kk, &vv, g.qt, reinterpret_cast<const int32_t*>(w.segs),
                          w.seg_count, g.seg_cap, g.dense_lo, g.dense_hi,
                          1.0f / sqrtf((float)g.d), a->out, a->out_dtype, a->out_row_stride,
                          a->out_head_stride, a->lse, a->err_flag, a->attn_kernel,
-                         past_tiles_estimate(a, g), stream);
+                         past_tiles_estimate(a, g), w.scratch, w.scratch_bytes, stream);
 }
 
 int lf_rowdot(const float* A, int32_t rows, int32_t d, const float* x, double* out, void* stream) {

@@ -49,10 +49,10 @@ __device__ __forceinline__ double dot_f32_dd(const float* __restrict__ row, cons
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int c = c0 + 4 * u;
-        dd_add(acc, (double)x[u].x * (double)qv[c]);
-        dd_add(acc, (double)x[u].y * (double)qv[c + 1]);
-        dd_add(acc, (double)x[u].z * (double)qv[c + 2]);
-        dd_add(acc, (double)x[u].w * (double)qv[c + 3]);
+        dd_add(acc, __dmul_rn(x[u].x, qv[c]));
+        dd_add(acc, __dmul_rn(x[u].y, qv[c + 1]));
+        dd_add(acc, __dmul_rn(x[u].z, qv[c + 2]));
+        dd_add(acc, __dmul_rn(x[u].w, qv[c + 3]));
       }
     }
   } else if ((d & 3) == 0 && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
@@ -131,10 +131,7 @@ __global__ void __launch_bounds__(128) select_kernel(SelArgs a) {
   // budget (selection.py:212-218, planner.py:119-123)
   const int current = a.f * a.bpf;
   int total = current;
-  if (a.chunk > 1) {
-    double s = *a.s_i;
-    total = (int)floor((1.0 - s) * (double)(a.chunk * current) + 0.5);
-  }
+  if (a.chunk > 1) total = budget_round(*a.s_i, (long long)a.chunk * current);
   const int past_budget = total > current ? total - current : 0;
   if (a.out_budget && w == 0 && lane == 0) {
     a.out_budget[0] = total;
@@ -277,7 +274,7 @@ __global__ void __launch_bounds__(128) select_cta_kernel(SelArgs a) {
 
   const int current = a.f * a.bpf;
   int total = current;
-  if (a.chunk > 1) total = (int)floor((1.0 - *a.s_i) * (double)(a.chunk * current) + 0.5);
+  if (a.chunk > 1) total = budget_round(*a.s_i, (long long)a.chunk * current);
   const int past_budget = total > current ? total - current : 0;
   if (a.out_budget && w == 0 && tid == 0) {
     a.out_budget[0] = total;

@@ -279,10 +279,13 @@ def past_tiles_hint(s_host, chunk: int, f: int, bpf: int, topk_frames: int,
 def attention(q, k, v, qt: TilingSpec, tiles: TilePlan | None, dense_lo: int, dense_hi: int,
               out: torch.Tensor | None = None, out_dtype=torch.float32, scale: float | None = None,
               lse: torch.Tensor | None = None, err: torch.Tensor | None = None,
-              kernel: int = L.LF_KERNEL_AUTO, past_tiles: int = -1) -> torch.Tensor:
+              kernel: int = L.LF_KERNEL_AUTO, past_tiles: int = -1,
+              scratch: torch.Tensor | None = None) -> torch.Tensor:
     """Block-sparse flash attention over bf16 [H, L, d] (d in {64, 128}).
 
-    kernel / past_tiles: lf_attention_ex's kernel choice and work hint."""
+    kernel / past_tiles: lf_attention_ex's kernel choice and work hint.
+    scratch: zero-filled uint8 buffer of lf_attention_scratch_bytes (the caller
+    owns it, one launch in flight per buffer); None = the device's library scratch."""
     lib = L.lib()
     H, Lq, d = q.shape
     if out is None:
@@ -291,12 +294,13 @@ def attention(q, k, v, qt: TilingSpec, tiles: TilePlan | None, dense_lo: int, de
     mq, mk, mv = L.mat(q), L.mat(k), L.mat(v)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
-    L.check(lib.lf_attention_ex(ctypes.byref(mq), ctypes.byref(mk), ctypes.byref(mv), qt.abi(),
+    L.check(lib.lf_attention_ws(ctypes.byref(mq), ctypes.byref(mk), ctypes.byref(mv), qt.abi(),
                                 tiles.segs.data_ptr() if tiles else None,
                                 tiles.seg_count.data_ptr() if tiles else None,
                                 tiles.seg_cap if tiles else 0, int(dense_lo), int(dense_hi),
                                 float(scale), out.data_ptr(), odt, out.stride(1), out.stride(0),
                                 L.ptr(lse), L.ptr(err), int(kernel), int(past_tiles),
+                                L.ptr(scratch), scratch.numel() if scratch is not None else 0,
                                 L.stream_ptr()))
     return out
 

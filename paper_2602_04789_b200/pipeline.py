@@ -91,7 +91,8 @@ class HsaPipeline:
         if nbytes == 0:
             L.check(L.LF_ERR_INVALID)
         if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            # zero-filled once: the attention scratch in it must start at zero (lfattn.h)
+            self._ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
         self._args = a
         self._bound = (q, k, v, s_i, out)
         self._graph = None

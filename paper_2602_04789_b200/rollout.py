@@ -24,6 +24,7 @@ import math
 
 import torch
 
+from . import _lib as L
 from . import device as D
 from .layout import ChunkLayout, as_layout, is_aligned
 from .planner import SparsityPlan
@@ -57,6 +58,12 @@ class HsaRollout:
         self.kf_cache = torch.zeros((H, lay.N * lay.f, d), dtype=torch.float32, device=self.device)
         self.committed = 0  # chunks whose clean K/V are in the cache
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # this rollout's attention split-KV scratch (zero-filled once, lfattn.h):
+        # independent of every other rollout / pipeline, also on other devices
+        nbytes = int(L.load_library().lf_attention_scratch_bytes(
+            H, L.tiling(lay.chunk_tokens, lay.n, lay.b_q), d))
+        with torch.cuda.device(self.device):
+            self.scratch = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
 
     # ------------------------------------------------------------------ helpers
     def _slot(self, i: int) -> slice:
@@ -197,15 +204,23 @@ class HsaRollout:
 
     def attend(self, plan: "StepPlan", out: torch.Tensor | None = None) -> torch.Tensor:
         """Attention half of a step: block-sparse attention of plan.q over the
-        cache (past chunks + the current chunk's K/V in its slot)."""
+        cache (past chunks + the current chunk's K/V in its slot).
+
+        The plan may come from ``prepare`` on another stream: its device
+        tensors are marked used by the current stream, so the caching allocator
+        cannot hand their memory to new work before this launch has run."""
         lay = self.layout
         i = plan.chunk
         P = (i - 1) * lay.f
         lk = lay.context_tokens(i)
+        cur = torch.cuda.current_stream()
+        for t in plan.device_tensors():
+            t.record_stream(cur)
         with D.qtile_scope(plan.qmode):
             return D.attention(plan.q, self.kv_k[:, :lk], self.kv_v[:, :lk], plan.qt, plan.tiles,
                                P * lay.n, lk, out=out, out_dtype=self.out_dtype,
-                               scale=1.0 / math.sqrt(lay.d), err=self.err, past_tiles=plan.hint)
+                               scale=1.0 / math.sqrt(lay.d), err=self.err, past_tiles=plan.hint,
+                               scratch=self.scratch)
 
 
 class StepPlan:
@@ -220,6 +235,13 @@ class StepPlan:
         self.tiles = tiles
         self.hint = hint
         self.qmode = qmode  # query-tile geometry the plan was made for (device.qtile_rows)
+
+    def device_tensors(self):
+        """The CUDA tensors attend() reads (for record_stream)."""
+        sel = self.selection
+        out = [self.q, self.q_block, self.tiles.segs, self.tiles.seg_count, sel.blocks, sel.count,
+               sel.frames, sel.budget]
+        return [t for t in out if t is not None and t.is_cuda]
 
 
 # --------------------------------------------------------------------------- ablation settings

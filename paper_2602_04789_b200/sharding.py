@@ -64,5 +64,9 @@ def gather_heads_overlapped(local: torch.Tensor, shard: HeadShard, out: torch.Te
     if shard.mode != "headshard":
         return
     comm_stream.wait_stream(torch.cuda.current_stream())
+    # both buffers are used on comm_stream: keep the caching allocator from
+    # recycling them for the current stream while the all-gather runs
+    local.record_stream(comm_stream)
+    out.record_stream(comm_stream)
     with torch.cuda.stream(comm_stream):
         gather_heads(local, shard, out=out, group=group)

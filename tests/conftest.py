@@ -26,3 +26,18 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture
+def lfopt():
+    """Set library options (include/lfattn.h LF_OPT_*) for one test; restored after.
+    The library reads its environment knobs once, so tests cannot use setenv."""
+    from paper_2602_04789_b200 import _lib as L
+    saved = []
+
+    def set_(name, value):
+        saved.append((name, L.set_option(name, int(value))))
+
+    yield set_
+    for name, prev in reversed(saved):
+        L.set_option(name, prev)

@@ -153,3 +153,36 @@ def test_reference_staged_for_gpu_box():
     names = sorted(x for x in os.listdir(make_ref.SRC) if x.endswith(".py"))
     match, mismatch, errors = filecmp.cmpfiles(make_ref.SRC, make_ref.DST, names, shallow=False)
     assert not mismatch and not errors and len(match) == len(names) == 8
+
+
+def test_options_roundtrip_without_gpu():
+    """lf_set_option / lf_get_option: the environment is read once, then the
+    cached value is what launch paths use; unknown options are rejected."""
+    from paper_2602_04789_b200 import _lib
+    lib = _lib.load_library()
+    for name, o in _lib.OPTIONS.items():
+        prev = lib.lf_get_option(o)
+        assert lib.lf_set_option(o, 3) == _lib.LF_OK and lib.lf_get_option(o) == 3
+        with _lib.option(name, 1):
+            assert lib.lf_get_option(o) == 1
+        assert lib.lf_get_option(o) == 3
+        lib.lf_set_option(o, prev)
+    assert lib.lf_set_option(99, 0) == _lib.LF_ERR_INVALID
+    assert lib.lf_get_option(99) == -2
+
+
+def test_pool_chunk_k_rejects_bad_output_strides():
+    """lf_pool_chunk_k validates its caller-provided output strides before any launch."""
+    import ctypes
+    from paper_2602_04789_b200 import _lib
+    lib = _lib.load_library()
+    H, f, n, d, b = 2, 3, 1560, 128, 64
+    bpf = -(-n // b)
+    k = _lib.LfMat(0x10000, _lib.LF_BF16, H, f * n, d, d, f * n * d)
+    t = _lib.tiling(f * n, n, b)
+    good_kb, good_kf = f * bpf * d, f * d
+    for kb_s, kf_s, kb_p in ((good_kb - 2, good_kf, 0x20000), (good_kb, good_kf - 2, 0x20000),
+                             (good_kb + 1, good_kf, 0x20000), (good_kb, good_kf, 0x20004)):
+        rc = lib.lf_pool_chunk_k(ctypes.byref(k), t, bpf, kb_p, kb_s, 0x40000, kf_s, None)
+        assert rc == _lib.LF_ERR_INVALID, (kb_s, kf_s, kb_p)
+        assert b"head strides" in lib.lf_last_error()

@@ -102,7 +102,7 @@ def test_kernel_choice_is_reported(lf):
 def test_plan_kernels_agree(lf, i, s_i, topk):
     # the 4-warp planner and the one-warp planner emit the same segment lists
     # (pads may carry a different, always valid, start row)
-    import os
+    from paper_2602_04789_b200 import _lib as L
     from paper_2602_04789_b200 import device as D
     from paper_2602_04789_b200.selection import tilings
     pipe, _, _ = _run(lf, TILE, 3, 1560, 3, i, 128, s_i, topk, seed=70 + i)
@@ -111,15 +111,11 @@ def test_plan_kernels_agree(lf, i, s_i, topk):
     P = (i - 1) * 3
     blocks, count, _, _ = pipe.selections()
     plans = []
-    for env in (None, "1"):
-        if env:
-            os.environ["LF_PLAN_WARP"] = env
-        try:
+    for warp in (0, 1):
+        with L.option("plan_warp", warp):
             t = D.plan_tiles(blocks, count, qt, kt, P * lay.frame_kv_blocks)
             torch.cuda.synchronize()
             plans.append((t.segs.cpu().numpy(), t.seg_count.cpu().numpy()))
-        finally:
-            os.environ.pop("LF_PLAN_WARP", None)
     (s0, c0), (s1, c1) = plans
     np.testing.assert_array_equal(c0, c1)
     for idx in np.ndindex(c0.shape):
@@ -130,3 +126,46 @@ def test_plan_kernels_agree(lf, i, s_i, topk):
         a[pad, 0] = 0
         b[pad, 0] = 0
         np.testing.assert_array_equal(a, b)
+
+
+def test_concurrent_calls_own_their_scratch(lf):
+    """Two hot-path calls in flight at once on two streams, each with its own
+    workspace (split-KV scratch included), give the results of running them
+    one after the other (lfattn.h: one call in flight per workspace, no
+    library-global scratch on the lf_hsa_forward path)."""
+    H, n, f, i, d = 2, 1560, 3, 5, 128  # 2 heads: every item is a split tail item
+    lay = lf.ChunkLayout(f=f, n=n, b_q=64, b_kv=64, d=d, N=7)
+    cfg = lf.SelectionConfig(topk_frames=6)
+    dev = torch.device("cuda")
+    cases = []
+    for seed, s_i in ((301, 0.5), (302, 0.7)):
+        q, k, v = O.synthetic_qkv(seed, f * n, i * f * n, d, heads=H)
+        t = [torch.from_numpy(a).to(dev, torch.bfloat16) for a in (q, k, v)]
+        cases.append((t, s_i))
+    seq = []
+    for t, s_i in cases:
+        pipe = lf.HsaPipeline(lay, H, i, cfg, framewise=True, out_dtype=torch.float32)
+        seq.append(pipe(*t, s_i).clone())
+    torch.cuda.synchronize()
+    pipes = [lf.HsaPipeline(lay, H, i, cfg, framewise=True, out_dtype=torch.float32)
+             for _ in cases]
+    outs = [p.bind(*t, s_i) for p, (t, s_i) in zip(pipes, cases)]
+    streams = [torch.cuda.Stream() for _ in cases]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for p, s in zip(pipes, streams):
+            with torch.cuda.stream(s):
+                p.launch()
+    torch.cuda.synchronize()
+    for p, o, ref in zip(pipes, outs, seq):
+        assert p.errors() == 0
+        assert torch.equal(o, ref)
+
+
+def test_rollouts_have_independent_attention_scratch(lf):
+    from paper_2602_04789_b200 import _lib as L
+    lay = lf.ChunkLayout(f=3, n=1560, b_q=64, b_kv=64, d=128, N=7)
+    a, b = (lf.HsaRollout(lay, 2) for _ in range(2))
+    assert a.scratch.data_ptr() != b.scratch.data_ptr()
+    assert a.scratch.numel() == L.lib().lf_attention_scratch_bytes(2, L.tiling(4680, 1560, 64), 128)
+    assert int(a.scratch.sum()) == 0

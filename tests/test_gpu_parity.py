@@ -62,9 +62,9 @@ def test_topk_indices(lf):
 
 @pytest.mark.parametrize("pool_cfg", ["2x4", "4x4", "4x8", "8x8"])
 @pytest.mark.parametrize("kind", ["aligned", "framewise"])
-def test_compress_bit_exact(lf, kind, pool_cfg, monkeypatch):
+def test_compress_bit_exact(lf, kind, pool_cfg, lfopt):
     # every (consumer groups x ring stages) variant of the TMA pooling kernel
-    monkeypatch.setenv("LF_POOL_CFG", pool_cfg)
+    lfopt("pool_cfg", {"2x4": 0, "4x4": 1, "4x8": 2, "8x8": 3}[pool_cfg])
     for m, arr in hsa_cases(kind):
         c = m["case"]
         if f"qb{c}" not in arr:
@@ -241,9 +241,9 @@ def test_compress_bf16_frame_path_bit_exact(lf, H, f, n, b, i, d):
 
 
 @pytest.mark.parametrize("split", ["1", "2", "3", "4"])
-def test_split_kv_merge(lf, split, monkeypatch):
+def test_split_kv_merge(lf, split, lfopt):
     # the split-KV load balancing (parts merged by the last finisher) must not change results
-    monkeypatch.setenv("LF_ATTN_SPLIT", split)
+    lfopt("attn_split", int(split))
     q, k, v = O.synthetic_qkv(21, 700, 3000, 128)
     out = lf.dense_attention(q[0], k[0], v[0])
     assert_close_attn(out, O.dense_attention(q[0], k[0], v[0]), f"split {split}")

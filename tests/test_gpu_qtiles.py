@@ -81,8 +81,8 @@ def test_block_tiles_close_to_row_tiles(lf):
 
 
 @pytest.mark.parametrize("split", ["1", "3"])
-def test_block_tiles_split_kv(lf, split, monkeypatch):
-    monkeypatch.setenv("LF_ATTN_SPLIT", split)
+def test_block_tiles_split_kv(lf, split, lfopt):
+    lfopt("attn_split", int(split))
     _pipeline_case(lf, 3, 1560, 3, 4, 128, 0.5, 6, "global", seed=5, check_heads=(1,))
 
 
@@ -99,15 +99,15 @@ def test_block_tiles_rollout(lf):
 # for block-aligned plans; the result must not depend on which CTA ran a unit.
 
 @pytest.mark.parametrize("split", [None, "3"])
-def test_dynamic_schedule_vs_oracle(lf, split, monkeypatch):
-    monkeypatch.setenv("LF_ATTN_DYNAMIC", "1")
+def test_dynamic_schedule_vs_oracle(lf, split, lfopt):
+    lfopt("attn_sched", 1)
     if split:
-        monkeypatch.setenv("LF_ATTN_SPLIT", split)
+        lfopt("attn_split", int(split))
     _pipeline_case(lf, 3, 1560, 3, 5, 128, 0.6, 6, "global", seed=55, check_heads=(0, 2))
 
 
-def test_dynamic_schedule_graph_replay(lf, monkeypatch):
-    monkeypatch.setenv("LF_ATTN_DYNAMIC", "1")
+def test_dynamic_schedule_graph_replay(lf, lfopt):
+    lfopt("attn_sched", 1)
     lay = lf.ChunkLayout(f=3, n=1560, b_q=64, b_kv=64, d=128, N=7)
     H, i = 5, 6
     q, k, v = O.synthetic_qkv(6, 3 * 1560, i * 3 * 1560, 128, heads=H)
@@ -122,8 +122,7 @@ def test_dynamic_schedule_graph_replay(lf, monkeypatch):
         pipe.replay()
         torch.cuda.synchronize()
         assert torch.equal(first, out)
-    monkeypatch.setenv("LF_ATTN_STATIC", "1")
-    monkeypatch.delenv("LF_ATTN_DYNAMIC")
+    lfopt("attn_sched", 0)
     pipe.launch()
     torch.cuda.synchronize()
     assert torch.equal(first, out)  # static round-robin: same result
