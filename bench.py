@@ -475,9 +475,9 @@ def run_ours(args, c):
 
         def run_sel(s=s, st=st):
             qb, kb, kf = st["views"]
-            sel = D.select(qb, kb, kf, bpf, i, f, c["topk"], c["mode"] == "per-frame", s_dev)
             with D.qtile_scope(qmode):
-                st["tiles"] = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf)
+                _, st["tiles"], _ = D.select_plan(qb, kb, kf, bpf, i, f, c["topk"],
+                                                  c["mode"] == "per-frame", s_dev, qt, kt, P * bpf)
 
         def run_attn(s=s, st=st):
             with D.qtile_scope(qmode):

@@ -160,6 +160,27 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
                   int32_t cap, lf_tiling q_tiling, lf_tiling k_tiling, int32_t list_blocks,
                   int32_t seg_cap, int32_t* segs, int32_t* seg_count, void* stream);
 
+/* Selection and tile plan of one step: lf_select_strided (with the optional
+ * top-k margin certificate) followed by lf_plan_tiles, same outputs.
+ *   out_margin  optional double [H][nqb][2]: per query block, the gap
+ *               min(selected score) - max(rejected score) of the frame and of
+ *               the block decision in the compensated fp64 scores the ordering
+ *               is defined on (per-frame mode: the smallest per-frame gap);
+ *               +inf where nothing was ranked (all kept / none).  A gap above
+ *               the fp64 error of any summation order of the reference's dot
+ *               products proves the reference selects the same sets
+ *               (selection.py:117-175, numerics.py:91-104).
+ *   list_blocks / seg_cap / segs / seg_count as lf_plan_tiles.               */
+int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_stride,
+                   const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
+                   int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+                   int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+                   const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+                   int32_t* out_count, int32_t* out_frames, int32_t* out_budget,
+                   double* out_margin, lf_tiling q_tiling, lf_tiling k_tiling,
+                   int32_t list_blocks, int32_t seg_cap, int32_t* segs, int32_t* seg_count,
+                   void* stream);
+
 /* Block-sparse flash attention (tcgen05 + TMEM + TMA, bf16 in, fp32 accum).
  * Query tile t of head h attends to its segments plus the dense key range
  * [dense_lo, dense_hi) (every row active), with -inf exclusion of masked keys.

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 
+#include <algorithm>
 #include <atomic>
 
 #include "attn_sm100_v5.cuh"
@@ -816,13 +817,14 @@ static int select_smem_per_warp(int d, int P, int frame_cap, int max_cand) {
   return (int)align_up(b, 16);
 }
 
-int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_head_stride,
-                      const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
-                      int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
-                      int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
-                      const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
-                      int32_t* out_count, int32_t* out_frames, double* out_scores,
-                      double* out_fscores, int32_t* out_budget, void* stream) {
+static int select_launch(const float* q_block, const float* k_block, int64_t kb_head_stride,
+                         const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
+                         int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+                         int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+                         const double* s_i_dev, int32_t cap, int32_t frame_cap,
+                         int32_t* out_blocks, int32_t* out_count, int32_t* out_frames,
+                         double* out_scores, double* out_fscores, int32_t* out_budget,
+                         double* out_margin, void* stream) {
   if (!q_block || !k_block || !s_i_dev || !out_blocks || !out_count || !out_frames)
     return fail(LF_ERR_INVALID, "lf_select: null pointer");
   if (heads < 1 || nqb < 1 || d < 1 || blocks_per_frame < 1 || chunk_index < 1 || frames_per_chunk < 1)
@@ -840,10 +842,11 @@ int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_hea
   SelArgs a{q_block, k_block, k_frame, heads, nqb, nkb, d, blocks_per_frame, chunk_index,
             frames_per_chunk, topk_frames, per_frame_mode ? 1 : 0, s_i_dev, cap, frame_cap,
             out_blocks, out_count, out_frames, out_scores, out_fscores, out_budget, wpc, spw,
-            max_cand, (long long)kb_head_stride, (long long)kf_head_stride};
+            max_cand, (long long)kb_head_stride, (long long)kf_head_stride, out_margin};
   // one 4-warp CTA per (head, query block); its working set adds the flags
   const int cta_smem = spw + (int)align_up((size_t)(P > max_cand ? P : max_cand), 16);
-  if (opt(LF_OPT_SELECT_WARP) != 1 && cta_smem <= 200 * 1024) {
+  if (out_margin || (opt(LF_OPT_SELECT_WARP) != 1 && cta_smem <= 200 * 1024)) {
+    if (cta_smem > 200 * 1024) return fail(LF_ERR_UNSUPPORTED, "selection working set too large");
     if (cta_smem > 48 * 1024)
       cudaFuncSetAttribute(select_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cta_smem);
     select_cta_kernel<<<heads * nqb, 128, cta_smem, S(stream)>>>(a);
@@ -855,6 +858,19 @@ int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_hea
   const int warps = heads * nqb;
   select_kernel<<<(warps + wpc - 1) / wpc, 32 * wpc, smem, S(stream)>>>(a);
   return check_launch("select_kernel");
+}
+
+int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_head_stride,
+                      const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
+                      int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+                      int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+                      const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+                      int32_t* out_count, int32_t* out_frames, double* out_scores,
+                      double* out_fscores, int32_t* out_budget, void* stream) {
+  return select_launch(q_block, k_block, kb_head_stride, k_frame, kf_head_stride, heads, nqb, nkb,
+                       d, blocks_per_frame, chunk_index, frames_per_chunk, topk_frames,
+                       per_frame_mode, s_i_dev, cap, frame_cap, out_blocks, out_count, out_frames,
+                       out_scores, out_fscores, out_budget, nullptr, stream);
 }
 
 int lf_select(const float* q_block, const float* k_block, const float* k_frame, int32_t heads,
@@ -920,6 +936,25 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
   const int warps = heads * ntiles;
   plan_tiles_kernel<<<(warps + wpc - 1) / wpc, 32 * wpc, smem, S(stream)>>>(a);
   return check_launch("plan_tiles_kernel");
+}
+
+int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_stride,
+                   const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
+                   int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
+                   int32_t frames_per_chunk, int32_t topk_frames, int32_t per_frame_mode,
+                   const double* s_i_dev, int32_t cap, int32_t frame_cap, int32_t* out_blocks,
+                   int32_t* out_count, int32_t* out_frames, int32_t* out_budget,
+                   double* out_margin, lf_tiling q_tiling, lf_tiling k_tiling,
+                   int32_t list_blocks, int32_t seg_cap, int32_t* segs, int32_t* seg_count,
+                   void* stream) {
+  int rc;
+  if ((rc = select_launch(q_block, k_block, kb_head_stride, k_frame, kf_head_stride, heads, nqb,
+                          nkb, d, blocks_per_frame, chunk_index, frames_per_chunk, topk_frames,
+                          per_frame_mode, s_i_dev, cap, frame_cap, out_blocks, out_count,
+                          out_frames, nullptr, nullptr, out_budget, out_margin, stream)))
+    return rc;
+  return lf_plan_tiles(out_blocks, out_count, heads, nqb, cap, q_tiling, k_tiling, list_blocks,
+                       seg_cap, segs, seg_count, stream);
 }
 
 int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
@@ -1056,12 +1091,12 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
   if ((rc = lf_compress(&a->q, &kview, g.qt, g.kt, g.bpf, g.P, w.q_block, w.k_block, w.k_frame,
                         stream)))
     return rc;
-  if ((rc = lf_select(w.q_block, w.k_block, w.k_frame, g.H, g.nqb, g.nkb, g.d, g.bpf,
-                      a->chunk_index, a->f, a->topk_frames, a->per_frame_mode, a->s_i_dev, g.cap,
-                      g.frame_cap, w.blocks, w.count, w.frames, nullptr, nullptr, w.budget, stream)))
-    return rc;
-  if ((rc = lf_plan_tiles(w.blocks, w.count, g.H, g.nqb, g.cap, g.qt, g.kt, g.list_blocks,
-                          g.seg_cap, reinterpret_cast<int32_t*>(w.segs), w.seg_count, stream)))
+  if ((rc = lf_select_plan(w.q_block, w.k_block, (int64_t)g.nkb * g.d, w.k_frame,
+                           (int64_t)g.P * g.d, g.H, g.nqb, g.nkb, g.d, g.bpf, a->chunk_index,
+                           a->f, a->topk_frames, a->per_frame_mode, a->s_i_dev, g.cap,
+                           g.frame_cap, w.blocks, w.count, w.frames, w.budget, nullptr, g.qt,
+                           g.kt, g.list_blocks, g.seg_cap, reinterpret_cast<int32_t*>(w.segs),
+                           w.seg_count, stream)))
     return rc;
   lf_mat kk = a->k, vv = a->v;
   kk.rows = vv.rows = a->chunk_index * a->f * a->n;

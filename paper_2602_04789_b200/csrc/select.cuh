@@ -35,6 +35,7 @@ struct SelArgs {
   int smem_per_warp;  // bytes
   int max_cand;
   long long kb_head_stride, kf_head_stride;  // elements (k_block / k_frame per head)
+  double* out_margin;  // optional [H][nqb][2] top-k margin certificate (select_cta_kernel)
 };
 
 __device__ __forceinline__ double dot_f32_dd(const float* __restrict__ row, const float* qv, int d) {
@@ -250,6 +251,25 @@ __global__ void topk_kernel(const double* sc, int n, int k, int* out_idx) {
 
 namespace lf {
 
+// CTA-wide min / max of per-thread doubles (128 threads; red = 8 doubles of
+// shared memory, reusable after the call)
+__device__ __forceinline__ void cta_minmax128(double& mn, double& mx, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = mn;
+    red[4 + warp] = mx;
+  }
+  __syncthreads();
+  mn = fmin(fmin(red[0], red[1]), fmin(red[2], red[3]));
+  mx = fmax(fmax(red[4], red[5]), fmax(red[6], red[7]));
+}
+
 // K2 with one 128-thread CTA per (head, query block): the same selection as
 // select_kernel (same scores, same ranks, same ascending output) with the
 // frame scores, candidate scores and ranks spread over four warps, so four
@@ -294,6 +314,18 @@ __global__ void __launch_bounds__(128) select_cta_kernel(SelArgs a) {
   const int kf_n = a.topk < P ? a.topk : P;
   for (int t = tid; t < P; t += 128) flag[t] = kf_n > 0 && (kf_n >= P || stable_rank(fsc, 0, P, t) < kf_n);
   __syncthreads();
+  __shared__ double mred[8];
+  double margin_f = INFINITY, margin_b = INFINITY;
+  if (a.out_margin && kf_n > 0 && kf_n < P) {
+    // frame decision gap: lowest selected score - highest rejected score
+    double mn = INFINITY, mx = -INFINITY;
+    for (int t = tid; t < P; t += 128) {
+      if (flag[t]) mn = fmin(mn, fsc[t]);
+      else mx = fmax(mx, fsc[t]);
+    }
+    cta_minmax128(mn, mx, mred);
+    margin_f = mn - mx;
+  }
   if (tid < 32) {  // ascending compaction
     int nsel = 0;
     for (int b0 = 0; b0 < P; b0 += 32) {
@@ -312,8 +344,15 @@ __global__ void __launch_bounds__(128) select_cta_kernel(SelArgs a) {
 
   const int bpf = a.bpf;
   const int C = nsel * bpf;
+  double* om = a.out_margin ? a.out_margin + 2 * ((size_t)h * a.nqb + r) : nullptr;
   if (C == 0 || past_budget == 0) {
-    if (tid == 0) a.out_count[w] = 0;
+    if (tid == 0) {
+      a.out_count[w] = 0;
+      if (om) {
+        om[0] = margin_f;
+        om[1] = margin_b;
+      }
+    }
     return;
   }
   int* ob = a.out_blocks + ((size_t)h * a.nqb + r) * a.cap;
@@ -342,6 +381,34 @@ __global__ void __launch_bounds__(128) select_cta_kernel(SelArgs a) {
     flag[c] = chosen;
   }
   __syncthreads();
+  if (om && (a.per_frame || budget < C)) {
+    // block decision gap (per-frame mode: the smallest of the per-frame gaps
+    // between rank per-1 and rank per; the budget truncation is positional)
+    if (!a.per_frame) {
+      double mn = INFINITY, mx = -INFINITY;
+      for (int c = tid; c < C; c += 128) {
+        if (flag[c]) mn = fmin(mn, csc[c]);
+        else mx = fmax(mx, csc[c]);
+      }
+      cta_minmax128(mn, mx, mred);
+      margin_b = mn - mx;
+    } else if (per < bpf) {
+      for (int fi = 0; fi < nsel; ++fi) {
+        double mn = INFINITY, mx = -INFINITY;
+        for (int c = fi * bpf + tid; c < (fi + 1) * bpf; c += 128) {
+          const bool in = stable_rank(csc, fi * bpf, bpf, c) < per;
+          if (in) mn = fmin(mn, csc[c]);
+          else mx = fmax(mx, csc[c]);
+        }
+        cta_minmax128(mn, mx, mred);
+        margin_b = fmin(margin_b, mn - mx);
+      }
+    }
+  }
+  if (om && tid == 0) {
+    om[0] = margin_f;
+    om[1] = margin_b;
+  }
   if (tid < 32) {
     int cnt = 0;
     for (int b0 = 0; b0 < C; b0 += 32) {

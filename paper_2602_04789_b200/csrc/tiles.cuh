@@ -133,6 +133,106 @@ __global__ void __launch_bounds__(128) plan_tiles_kernel(PlanArgs a) {
 
 namespace lf {
 
+// Segment emission of one plan tile, shared by plan_tiles_cta_kernel and the
+// fused selection + plan kernel (select_plan.cuh): qm[b] (shared memory) = the
+// query-block bitmask of past key block b.  NW warps each own a contiguous
+// range of key blocks; a counting pass gives every warp its output offsets in
+// each class, a second pass writes.  Classes 3 (both 128-row halves), 1 (first
+// only), 2 (second only), in ascending key order, each padded to an even count
+// in pair mode with {0, 0, 0, 0}.  The output does not depend on NW.  Called
+// by all NW*32 threads (contains __syncthreads).
+template <int NW>
+__device__ void emit_plan_segments(const unsigned int* qm, int list_blocks, const Tiling& kt,
+                                   unsigned int maskA, unsigned int maskB, bool pairs,
+                                   int4* out, int seg_cap, int* seg_count_out,
+                                   int (*cnt)[4]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per_w = (list_blocks + NW - 1) / NW;
+  const int bw0 = warp * per_w;
+  int bw1 = bw0 + per_w;
+  bw1 = bw1 < list_blocks ? bw1 : list_blocks;
+  auto classify = [&](int b, unsigned int& m, int& c, int& s, int& e, int& pieces) {
+    m = b < bw1 ? qm[b] : 0u;
+    c = m ? (((m & maskA) ? 1 : 0) | ((m & maskB) ? 2 : 0)) : 0;
+    pieces = 0;
+    if (c) {
+      s = kt.start(b);
+      e = kt.end(b);
+      pieces = (e - s + kSegKeys - 1) / kSegKeys;
+    }
+  };
+  // counting pass
+  int my[4] = {0, 0, 0, 0};
+  for (int b0 = bw0; b0 < bw1; b0 += 32) {
+    unsigned int m;
+    int c, s, e, pieces;
+    classify(b0 + lane, m, c, s, e, pieces);
+#pragma unroll
+    for (int k = 1; k <= 3; ++k) {
+      int v = c == k ? pieces : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      my[k] += v;
+    }
+  }
+  if (lane == 0)
+    for (int k = 1; k <= 3; ++k) cnt[warp][k] = my[k];
+  __syncthreads();
+  // class order: 3 (both halves), 1 (first), 2 (second), each padded to even in pair mode
+  int base[4], total[4];
+  {
+    int off = 0;
+    const int order[3] = {3, 1, 2};
+    for (int oi = 0; oi < 3; ++oi) {
+      const int k = order[oi];
+      total[k] = 0;
+      for (int ww = 0; ww < NW; ++ww) total[k] += cnt[ww][k];
+      base[k] = off;
+      off += total[k] + (pairs && (total[k] & 1) ? 1 : 0);
+    }
+    base[0] = off;  // segment count
+  }
+  int run[4];
+  for (int k = 1; k <= 3; ++k) {
+    run[k] = base[k];
+    for (int ww = 0; ww < warp; ++ww) run[k] += cnt[ww][k];
+  }
+  for (int b0 = bw0; b0 < bw1; b0 += 32) {
+    unsigned int m;
+    int c, s, e, pieces;
+    classify(b0 + lane, m, c, s, e, pieces);
+#pragma unroll
+    for (int k = 1; k <= 3; ++k) {
+      const int v = c == k ? pieces : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (v) {
+        const int off = run[k] + incl - v;
+        for (int p = 0; p < v; ++p) {
+          const int pos = off + p;
+          if (pos < seg_cap) {
+            const int st = s + p * kSegKeys;
+            const int ln = e - st < kSegKeys ? e - st : kSegKeys;
+            out[pos] = make_int4(st, ln, (int)m, 0);
+          }
+        }
+      }
+      run[k] += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  if (tid == 0) {
+    if (pairs)
+      for (int k = 1; k <= 3; ++k)
+        if ((total[k] & 1) && base[k] + total[k] < seg_cap)
+          out[base[k] + total[k]] = make_int4(0, 0, 0, 0);
+    *seg_count_out = base[0] < seg_cap ? base[0] : seg_cap;
+  }
+}
+
 // plan_tiles_kernel with one 128-thread CTA per (head, plan tile): the key
 // blocks are split into four contiguous ranges, one per warp; a counting pass
 // gives every warp its output offsets in each class, a second pass writes.
@@ -140,7 +240,7 @@ namespace lf {
 // positions; a pad's start is 0, any valid key row).
 __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   extern __shared__ unsigned int qm[];
-  __shared__ int cnt[4][4];  // [warp][class 1..3]
+  __shared__ int cnt[4][4];  // [warp][class 1..3] (emit_plan_segments)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int w = blockIdx.x;
   const int h = w / a.ntiles, t = w - h * a.ntiles;
@@ -184,91 +284,8 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   const bool pairs = a.qmode || a.tile_rows != kTileRows;
   const unsigned int maskA = pairs ? bits(q0, mid) : 0xffffffffu;
   const unsigned int maskB = pairs ? bits(mid, q1) : 0u;
-  // this warp's key-block range
-  const int per_w = (a.list_blocks + 3) / 4;
-  const int bw0 = warp * per_w;
-  int bw1 = bw0 + per_w;
-  bw1 = bw1 < a.list_blocks ? bw1 : a.list_blocks;
-  auto classify = [&](int b, unsigned int& m, int& c, int& s, int& e, int& pieces) {
-    m = b < bw1 ? qm[b] : 0u;
-    c = m ? (((m & maskA) ? 1 : 0) | ((m & maskB) ? 2 : 0)) : 0;
-    pieces = 0;
-    if (c) {
-      s = a.kt.start(b);
-      e = a.kt.end(b);
-      pieces = (e - s + kSegKeys - 1) / kSegKeys;
-    }
-  };
-  // counting pass
-  int my[4] = {0, 0, 0, 0};
-  for (int b0 = bw0; b0 < bw1; b0 += 32) {
-    unsigned int m;
-    int c, s, e, pieces;
-    classify(b0 + lane, m, c, s, e, pieces);
-#pragma unroll
-    for (int k = 1; k <= 3; ++k) {
-      int v = c == k ? pieces : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      my[k] += v;
-    }
-  }
-  if (lane == 0)
-    for (int k = 1; k <= 3; ++k) cnt[warp][k] = my[k];
-  __syncthreads();
-  // class order: 3 (both halves), 1 (first), 2 (second), each padded to even in pair mode
-  int base[4], total[4];
-  {
-    int off = 0;
-    const int order[3] = {3, 1, 2};
-    for (int oi = 0; oi < 3; ++oi) {
-      const int k = order[oi];
-      total[k] = cnt[0][k] + cnt[1][k] + cnt[2][k] + cnt[3][k];
-      base[k] = off;
-      off += total[k] + (pairs && (total[k] & 1) ? 1 : 0);
-    }
-    base[0] = off;  // segment count
-  }
-  int4* out = a.segs + (size_t)w * a.seg_cap;
-  int run[4];
-  for (int k = 1; k <= 3; ++k) {
-    run[k] = base[k];
-    for (int ww = 0; ww < warp; ++ww) run[k] += cnt[ww][k];
-  }
-  for (int b0 = bw0; b0 < bw1; b0 += 32) {
-    unsigned int m;
-    int c, s, e, pieces;
-    classify(b0 + lane, m, c, s, e, pieces);
-#pragma unroll
-    for (int k = 1; k <= 3; ++k) {
-      const int v = c == k ? pieces : 0;
-      int incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-      }
-      if (v) {
-        const int off = run[k] + incl - v;
-        for (int p = 0; p < v; ++p) {
-          const int pos = off + p;
-          if (pos < a.seg_cap) {
-            const int st = s + p * kSegKeys;
-            const int ln = e - st < kSegKeys ? e - st : kSegKeys;
-            out[pos] = make_int4(st, ln, (int)m, 0);
-          }
-        }
-      }
-      run[k] += __shfl_sync(0xffffffffu, incl, 31);
-    }
-  }
-  if (tid == 0) {
-    if (pairs)
-      for (int k = 1; k <= 3; ++k)
-        if ((total[k] & 1) && base[k] + total[k] < a.seg_cap)
-          out[base[k] + total[k]] = make_int4(0, 0, 0, 0);
-    a.seg_count[w] = base[0] < a.seg_cap ? base[0] : a.seg_cap;
-  }
+  emit_plan_segments<4>(qm, a.list_blocks, a.kt, maskA, maskB, pairs,
+                        a.segs + (size_t)w * a.seg_cap, a.seg_cap, a.seg_count + w, cnt);
 }
 
 }  // namespace lf

@@ -258,6 +258,48 @@ def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
     return TilePlan(segs, seg_count, seg_cap)
 
 
+def select_plan(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: int,
+                per_frame: bool, s_i, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
+                want_margin: bool = False):
+    """select() + plan_tiles() of one step (lf_select_plan).  Returns
+    (Selections, TilePlan, margin) with margin = [H, nqb, 2] fp64 top-k margin
+    certificate (frames, blocks) or None."""
+    lib = L.lib()
+    H, nqb, d = q_block.shape
+    nkb = k_block.shape[1]
+    P = (chunk - 1) * f
+    kf = min(topk, P)
+    cap = max(1, kf * bpf)
+    frame_cap = max(1, kf)
+    dev = q_block.device
+    if not torch.is_tensor(s_i):
+        s_i = torch.tensor([float(s_i)], dtype=torch.float64, device=dev)
+    for t in (q_block, k_block, k_frame):
+        assert t.stride(2) == 1 and t.stride(1) == d, "summaries must have contiguous rows"
+    blocks = torch.empty((H, nqb, cap), dtype=torch.int32, device=dev)
+    count = torch.empty((H, nqb), dtype=torch.int32, device=dev)
+    frames = torch.empty((H, nqb, frame_cap), dtype=torch.int32, device=dev)
+    budget = torch.zeros(4, dtype=torch.int32, device=dev)
+    margin = torch.empty((H, nqb, 2), dtype=torch.float64, device=dev) if want_margin else None
+    rows = plan_rows()
+    ntiles = int(lib.lf_plan_tile_count(qt.abi()))
+    mq = 4 if qtile_mode(qt) else qt.max_blocks_per_tile(rows)
+    pieces = -(-kt.block // SEG_KEYS)
+    seg_cap = max(1, min(mq * cap * pieces, max(list_blocks, 0) * pieces)
+                  + (3 if rows > TILE_ROWS else 0))
+    segs = torch.empty((H, ntiles, seg_cap, 4), dtype=torch.int32, device=dev)
+    seg_count = torch.empty((H, ntiles), dtype=torch.int32, device=dev)
+    L.check(lib.lf_select_plan(q_block.data_ptr(), k_block.data_ptr(), k_block.stride(0),
+                               k_frame.data_ptr() if P > 0 else None,
+                               k_frame.stride(0) if P > 0 else 0, H, nqb, nkb, d, int(bpf),
+                               int(chunk), int(f), int(topk), 1 if per_frame else 0,
+                               s_i.data_ptr(), cap, frame_cap, blocks.data_ptr(),
+                               count.data_ptr(), frames.data_ptr(), budget.data_ptr(),
+                               L.ptr(margin), qt.abi(), kt.abi(), int(list_blocks), int(seg_cap),
+                               segs.data_ptr(), seg_count.data_ptr(), L.stream_ptr()))
+    return (Selections(blocks, count, frames, budget), TilePlan(segs, seg_count, seg_cap), margin)
+
+
 def past_tiles_hint(s_host, chunk: int, f: int, bpf: int, topk_frames: int,
                     qt: TilingSpec) -> int:
     """Estimated non-dense 128-key tiles per 256-row plan tile (the work hint of

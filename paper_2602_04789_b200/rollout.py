@@ -187,15 +187,16 @@ class HsaRollout:
         P = (i - 1) * lay.f
         q_block = D.pool_blocks(q, qt)
         s_dev = self._s_dev(i, s_i)
-        sel = D.select(q_block, self.kb_cache, self.kf_cache, self.bpf, i, lay.f,
-                       self.cfg.topk_frames, self.cfg.block_budget_mode == "per-frame", s_dev)
         if s_host is None and s_i is not None and not torch.is_tensor(s_i):
             s_host = float(s_i)
         if s_host is None and s_i is None and self.plan is not None:
             s_host = float(self.plan.s[i - 1])
         # query-tile geometry of this step (block-aligned when the past selection is large)
         with D.qtile_scope(D.auto_qtile_mode(s_host, i, lay.f, self.bpf, self.cfg.topk_frames)):
-            tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * self.bpf)
+            sel, tiles, _ = D.select_plan(q_block, self.kb_cache, self.kf_cache, self.bpf, i,
+                                          lay.f, self.cfg.topk_frames,
+                                          self.cfg.block_budget_mode == "per-frame", s_dev, qt,
+                                          kt, P * self.bpf)
             qmode = D.qtile_mode(qt)
         hint = D.past_tiles_hint(s_host, i, lay.f, self.bpf, self.cfg.topk_frames, qt)
         self.last_selection = sel

@@ -237,9 +237,9 @@ def hsa_attention(q, k, v, chunk_index: int, s_i: float, cfg: SelectionConfig,
 
     with _Timer() as t_sel:
         qb, kb, kf = D.compress(qd[None], kd[None], qt, kt, bpf, P)
-        sel = D.select(qb, kb, kf, bpf, chunk_index, layout.f, cfg.topk_frames,
-                       cfg.block_budget_mode == "per-frame", s_dev)
-        tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, list_blocks=P * bpf)
+        sel, tiles, _ = D.select_plan(qb, kb, kf, bpf, chunk_index, layout.f, cfg.topk_frames,
+                                      cfg.block_budget_mode == "per-frame", s_dev, qt, kt,
+                                      P * bpf)
     qh, kh, vh = C.to_bf16_heads(qd), C.to_bf16_heads(kd), C.to_bf16_heads(vd)
     with _Timer() as t_att:
         out = D.attention(qh, kh, vh, qt, tiles, P * layout.n, ctx, out_dtype=torch.float32,

@@ -157,7 +157,9 @@ def test_plans_on_device(lf):
         np.testing.assert_allclose(p.achieved_flops_ratio, rec["achieved"], rtol=1e-12)
 
 
-def _pipeline_case(lf, H, n, f, i, d, s_i, topk, mode, seed, check_heads):
+def _pipeline_case(lf, H, n, f, i, d, s_i, topk, mode, seed, check_heads, mask_heads=()):
+    """HsaPipeline (lf_hsa_forward) on seeded inputs: masks of check_heads and
+    mask_heads bit-exact against the oracle, outputs of check_heads in tolerance."""
     lay = lf.ChunkLayout(f=f, n=n, b_q=64, b_kv=64, d=d, N=max(i, 7))
     cfg = lf.SelectionConfig(topk_frames=topk, block_budget_mode=mode)
     q, k, v = O.synthetic_qkv(seed, f * n, i * f * n, d, heads=H)
@@ -170,7 +172,10 @@ def _pipeline_case(lf, H, n, f, i, d, s_i, topk, mode, seed, check_heads):
     torch.cuda.synchronize()
     assert pipe.errors() == 0
     masks = pipe.masks()
-    fw = not lay.aligned or True
+    fw = True
+    for h in sorted(set(mask_heads) - set(check_heads)):
+        _, sel = O.select(q[h], k[h], i, s_i, f, n, 64, 64, topk, mode, framewise=fw)
+        np.testing.assert_array_equal(masks[h].bits, sel.bits, err_msg=f"head {h}")
     for h in check_heads:
         views, sel = O.select(q[h], k[h], i, s_i, f, n, 64, 64, topk, mode, framewise=fw)
         np.testing.assert_array_equal(masks[h].bits, sel.bits, err_msg=f"head {h}")
@@ -193,6 +198,25 @@ def test_pipeline_long_rollout_chunk14(lf):
     plan = lf.allocate(0.9, 0.98, 21, 4, lay)
     s14 = plan.s[13]
     _pipeline_case(lf, 4, 1560, 3, 14, 128, s14, 6, "global", seed=1414, check_heads=(0, 3))
+
+
+def test_pipeline_long_rollout_chunk21(lf):
+    # BASELINE config 3 at chunk 21 of the N=21 CAG plan: 60 past frames, past
+    # budget 53; all 12 heads' masks bit-exact, outputs of two heads in tolerance
+    lay = lf.ChunkLayout(f=3, n=1560, b_q=64, b_kv=64, d=128, N=21)
+    plan = lf.allocate(0.9, 0.98, 21, 4, lay)
+    assert plan.budgets[20] - 75 == 53
+    pipe = _pipeline_case(lf, 12, 1560, 3, 21, 128, plan.s[20], 6, "global", seed=2121,
+                          check_heads=(0, 11), mask_heads=range(12))
+    assert int(pipe.selections()[3][1]) == 53
+
+
+@pytest.mark.parametrize("s_i", [6 / 7, 0.5])
+def test_pipeline_config4_heads40(lf, s_i):
+    # BASELINE config 4: Wan-14B attention shape, 40 heads x d128 at chunk 7
+    # (6/7 = the CAG plan's s_7: current chunk only; 0.5 selects past blocks)
+    _pipeline_case(lf, 40, 1560, 3, 7, 128, s_i, 6, "global", seed=4040,
+                   check_heads=(0, 17, 39), mask_heads=range(40))
 
 
 def test_pipeline_config1_shape(lf):
