@@ -164,6 +164,21 @@ def host_s(lf, c, lay):
     return p.s[c["chunk"] - 1]
 
 
+def job_config(args, c, s_i, world):
+    """The workload's config dict, identical in both arms (ours / --impl reference)."""
+    from paper_2602_04789_b200.sharding import partition_heads
+    H, d, n, f, i, T = c["heads"], c["d"], c["n"], c["f"], c["chunk"], c["T"]
+    lk = i * f * n
+    return {"workload": f"{args.config}: {H} heads x d{d}, n={n} tokens/frame (framewise "
+                        f"b=64), f={f}, chunk {i} of {c['N']}, T={T} calls/step",
+            "heads": H, "d": d, "n": n, "f": f, "chunk": i, "N": c["N"], "T": T,
+            "plan": list(c["plan"]) if c["plan"] else None, "s_i": s_i,
+            "topk_frames": c["topk"], "mode": c["mode"],
+            "parallelism": partition_heads(H, world, 0).mode,
+            "l2": f"inputs larger than L2 (K+V per call {2 * H * lk * d * 2 / 1e6:.0f} MB "
+                  f"over all heads)"}
+
+
 # ---------------------------------------------------------------------------- CPU legs
 
 
@@ -182,7 +197,36 @@ def oracle_sample(c, s_i, seed, threads):
     return dt, flops
 
 
+def ref_aligned_sample(c, s_i, seed, threads):
+    """Time the REAL reference (chunkattn.hsa_attention, staged unmodified in
+    oracle/_ref) on one head at the aligned n = 1536 form of the workload (the
+    reference rejects n = 1560, selection.py:88-92).  None if not staged."""
+    import numpy as np
+    from oracle import lf_oracle as O
+    from oracle.make_ref import import_reference
+    try:
+        R = import_reference()
+    except ImportError:
+        return None
+    i, f, d = c["chunk"], c["f"], c["d"]
+    n = c["n"] - c["n"] % 64
+    lay = R.ChunkLayout(f=f, n=n, b_q=64, b_kv=64, d=d, N=c["N"])
+    cfg = R.SelectionConfig(topk_frames=c["topk"], block_budget_mode=c["mode"])
+    q, k, v = O.synthetic_qkv(seed, f * n, i * f * n, d)
+    t0 = time.perf_counter()
+    out, st, _ = R.hsa_attention(q[0], k[0], v[0], i, s_i, cfg, lay, threads=threads)
+    dt = time.perf_counter() - t0
+    assert np.isfinite(out).all()
+    return dt, 2 * st.flop_estimate, n  # aligned 64x64 tiles: effective = 2 x MAC count
+
+
 def run_reference(args, c):
+    """The reference arm: the reference's own CPU implementation of the path on
+    this box's host cores -- the unmodified chunkattn.hsa_attention staged in
+    oracle/_ref, at the aligned n = 1536 form of the workload (it rejects
+    n = 1560, selection.py:88-92), one head-call per step, all host threads;
+    the framewise oracle port at the workload's own n is timed beside it.
+    Without a staged reference the port is the arm's value."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -190,29 +234,53 @@ def run_reference(args, c):
     lay = make_layout(lf, c)
     s_i = host_s(lf, c, lay)
     threads = os.cpu_count() or 1
+    real = ref_aligned_sample(c, s_i, 99, threads) is not None  # also the first warm-up
     for w in range(args.warmup):
-        oracle_sample(c, s_i, 100 + w, threads)
+        if real:
+            ref_aligned_sample(c, s_i, 100 + w, threads)
+        else:
+            oracle_sample(c, s_i, 100 + w, threads)
     times, flops = [], []
     for st in range(args.steps):
-        dt, fl = oracle_sample(c, s_i, 1000 + st, threads)
+        if real:
+            dt, fl, n_al = ref_aligned_sample(c, s_i, 1000 + st, threads)
+        else:
+            dt, fl = oracle_sample(c, s_i, 1000 + st, threads)
         times.append(dt)
         flops.append(fl)
-    tot_t = sum(times)
-    value = sum(flops) / tot_t / 1e12
+    value = sum(flops) / sum(times) / 1e12
     ms_chunk = statistics.mean(times) * c["heads"] * c["T"] * 1e3
-    sample = (f"1 head of 1 denoising-step call of chunk {c['chunk']} per step (oracle port of "
-              f"chunkattn.hsa_attention, framewise n={c['n']}), OPENBLAS_NUM_THREADS=1, "
-              f"threads={threads}; ms/chunk extrapolated x{c['heads']} heads x{c['T']} steps")
+    if real:
+        kind = "reference"
+        sample = (f"1 head of 1 denoising-step call of chunk {c['chunk']} per step through the "
+                  f"unmodified chunkattn.hsa_attention (oracle/_ref) at the aligned n={n_al} "
+                  f"(the reference rejects n={c['n']}), OPENBLAS_NUM_THREADS=1, "
+                  f"threads={threads}; ms/chunk extrapolated x{c['heads']} heads x{c['T']} steps")
+    else:
+        kind = "port"
+        sample = (f"1 head of 1 denoising-step call of chunk {c['chunk']} per step (oracle port "
+                  f"of chunkattn.hsa_attention, framewise n={c['n']}), OPENBLAS_NUM_THREADS=1, "
+                  f"threads={threads}; ms/chunk extrapolated x{c['heads']} heads x{c['T']} steps")
+    port = None
+    if real:  # the framewise port at the workload's own n, beside it
+        pt, pf = 0.0, 0
+        for j in range(max(1, min(args.steps, 3))):
+            dt, fl = oracle_sample(c, s_i, 2000 + j, threads)
+            pt += dt
+            pf += fl
+        port = {"value": pf / pt / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": f"framewise oracle port at n={c['n']}, "
+                          f"{max(1, min(args.steps, 3))} head-call(s)"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.mean(times) * 1e3, "ms_per_chunk": ms_chunk,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
         "data": "synthetic",
-        "config": {"workload": args.config, **{k: v for k, v in c.items() if k != "plan"},
-                   "plan": list(c["plan"]) if c["plan"] else None, "s_i": s_i},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "config": job_config(args, c, s_i, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": sample, "cpu": cpu_desc()},
+        "port_framewise": port,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -537,6 +605,7 @@ def run_ours(args, c):
     achieved_tf = flops_call / (attn_ms * 1e-3) / 1e12
     pool_bytes = h_local * (lq + lk) * d * 2 + h_local * (qt.count + kt.count + P) * d * 4
     achieved_gbs = pool_bytes / (pool_ms * 1e-3) / 1e9
+    stage_gbs = pool_bytes / ((pool_ms + sel_ms) * 1e-3) / 1e9
 
     # ---- end to end through the public API with pinned host buffers, H2D of
     # every step's inputs and D2H of its output inside the timed region
@@ -657,18 +726,42 @@ def run_ours(args, c):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
+        # the real reference (oracle/_ref) at the aligned n, ~10 s of head-calls
+        real = ref_aligned_sample(c, s_host, 4141, threads)
+        if real is not None:
+            tot_t, tot_f, calls = real[0], real[1], 1
+            while calls < H * T and tot_t < 10.0:
+                dt, fl, n_al = ref_aligned_sample(c, s_host, 4242 + calls, threads)
+                tot_t += dt
+                tot_f += fl
+                calls += 1
+            cpu = {"value": tot_f / tot_t / 1e12, "unit": UNIT, "cores": threads,
+                   "kind": "reference",
+                   "sample": (f"{calls} of the {H * T} head-calls of one chunk-{i} step through "
+                              f"the unmodified chunkattn.hsa_attention (oracle/_ref) at the "
+                              f"aligned n={real[2]} (it rejects n={n}), {tot_t:.1f} s; "
+                              f"OPENBLAS_NUM_THREADS=1, threads={threads}"),
+                   "ms_per_chunk": tot_t / calls * H * T * 1e3,
+                   "ms_per_chunk_is_extrapolated": calls < H * T, "cpu": cpu_desc()}
+        # the framewise oracle port at the workload's own n (the value when no
+        # reference is staged, else beside it on a smaller sample)
         tot_t, tot_f, calls = 0.0, 0, 0
-        while calls < H * T and tot_t < 10.0:
+        budget_s = 10.0 if cpu is None else 3.0
+        while calls < H * T and tot_t < budget_s:
             dt, cflops = oracle_sample(c, s_host, 4242 + calls, threads)
             tot_t += dt
             tot_f += cflops
             calls += 1
-        cpu = {"value": tot_f / tot_t / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": (f"{calls} of the {H * T} head-calls of one chunk-{i} step (framewise "
-                          f"oracle port of chunkattn.hsa_attention), {tot_t:.1f} s; "
-                          f"OPENBLAS_NUM_THREADS=1, threads={threads}"),
-               "ms_per_chunk": tot_t / calls * H * T * 1e3,
-               "ms_per_chunk_is_extrapolated": calls < H * T, "cpu": cpu_desc()}
+        port = {"value": tot_f / tot_t / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": (f"{calls} of the {H * T} head-calls of one chunk-{i} step (framewise "
+                           f"oracle port of chunkattn.hsa_attention), {tot_t:.1f} s; "
+                           f"OPENBLAS_NUM_THREADS=1, threads={threads}"),
+                "ms_per_chunk": tot_t / calls * H * T * 1e3,
+                "ms_per_chunk_is_extrapolated": calls < H * T, "cpu": cpu_desc()}
+        if cpu is None:
+            cpu = port
+        else:
+            cpu["port_framewise"] = port
 
     # PCIe bound of the e2e leg: the step's H2D copies alone (same pinned
     # buffers, same order), timed on the device
@@ -694,17 +787,10 @@ def run_ours(args, c):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_chunk_r,
             "ms_per_chunk": ms_chunk_r, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {H} heads x d{d}, n={n} tokens/frame "
-                                   f"(framewise b=64), f={f}, chunk {i} of {c['N']}, "
-                                   f"T={T} calls/step",
-                       "heads": H, "d": d, "n": n, "f": f, "chunk": i, "N": c["N"],
-                       "plan": list(c["plan"]) if c["plan"] else None, "s_i": s_host,
-                       "topk_frames": c["topk"], "mode": c["mode"], "parallelism": mode,
-                       "query_tiles": ("block-aligned (2 query blocks)" if (
-                           os.environ.get("LF_QTILE", "") == "blocks" or (
-                               not os.environ.get("LF_QTILE") and qmode)) else "128-row"),
-                       "l2": "inputs larger than L2 (K+V per call "
-                             f"{2 * h_local * lk * d * 2 / 1e6:.0f} MB)"},
+            "config": job_config(args, c, s_host, world),
+            "query_tiles": ("block-aligned (2 query blocks)" if (
+                os.environ.get("LF_QTILE", "") == "blocks" or (
+                    not os.environ.get("LF_QTILE") and qmode)) else "128-row"),
             "e2e": {"value": flops_r_step / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                     "ms_per_chunk": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "HsaRollout.commit + prepare/attend (C ABI underneath); H2D, selection, attention and D2H on four streams",
@@ -729,13 +815,20 @@ def run_ours(args, c):
                          "issued_frac": mma_call / (attn_ms * 1e-3) / 1e12 / tf_peak,
                          "note": "achieved counts the selection's FLOPs; issued counts the "
                                  "128x128 tiles the tile plan makes the kernel compute"},
-            "roofline_select": {"bound": "hbm", "kernel": "pool_frames_tma_kernel (Q+K block pooling)",
-                                "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                                "frac": achieved_gbs / hbm_peak, "peak_source": hbm_src,
+            "roofline_select": {"bound": "hbm",
+                                "kernel": "mask-selection stage: pool_frames_tma_kernel (Q+K block "
+                                          "pooling) + select_cta_kernel + plan_tiles_cta_kernel",
+                                "achieved": stage_gbs, "peak": hbm_peak, "unit": "GB/s",
+                                "frac": stage_gbs / hbm_peak, "peak_source": hbm_src,
                                 "traffic": (traffic.get("pool", {}).get("bytes")
                                             if args.config == "c2" else None),
                                 "bytes_per_call": pool_bytes,
-                                "pool_ms_per_call": pool_ms, "select_plan_ms_per_call": sel_ms},
+                                "stage_ms_per_call": pool_ms + sel_ms,
+                                "pool_ms_per_call": pool_ms, "select_plan_ms_per_call": sel_ms,
+                                "pool_gbs": achieved_gbs, "pool_frac": achieved_gbs / hbm_peak,
+                                "note": "achieved = the stage's algorithmic HBM bytes (bf16 Q and "
+                                        "K reads + fp32 summary writes) / (pool + select + plan "
+                                        "time); selection and plan read the summaries from L2"},
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches_per_chunk * args.steps,
@@ -747,9 +840,37 @@ def run_ours(args, c):
         dist.destroy_process_group()
 
 
+def self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 with the same arguments; rank 0 prints
+    the line.  Refuses (non-zero exit, reason on stderr) when the node has
+    fewer than N GPUs -- never a silent single-GPU run."""
+    n = args.gpus
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            sys.stderr.write(f"bench.py: --gpus {n} needs {n} CUDA devices, this node has {have}\n")
+            return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     c = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(self_launch(args))
+    if world and world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, c)
     else:
