@@ -1,44 +1,47 @@
-// K4 v7: one 128-row query tile per CTA, two softmax sets on alternating key
-// tiles (ping-pong inside the tile).
+// K4 v8: one 128-row query tile per CTA; each 128-key tile is split between two
+// softmax sets (set X takes the tile's 64-key segment X), and every set's S is
+// double-buffered in TMEM, so the tensor core computes QK of tile k+1 while the
+// sets run the softmax of tile k.
 //
 // Contract: attention.py:168-188, 229-274 restated (see attn_common.cuh).
-// The tile kernel (v3) ran one online softmax per query tile: each key tile's
-// softmax waited on the previous one's.  The pair kernel (v5) ping-pongs two
-// query tiles but needs pair items (and a stream-K tail when the items do not
-// fill the grid).  Here the k-th needed key tile of a query tile goes to
-// softmax set k & 1; each set keeps its own running max / sum and its own O
-// accumulator in TMEM, and the two partial states are merged exactly when the
-// tile ends (split-KV identity inside the CTA).  Work items are v3's
-// (head, 128-row tile) with its split tail, so c2's 444 tiles fill the 148
-// SMs three times without merges.
+// Why: in v7 (sets on alternating 128-key tiles, one S buffer each) a set's
+// chain softmax(k) -> PV(k) -> QK(k+2) -> softmax(k+2) is serial, so the tensor
+// pipe idles while both sets wait (measured ~60-65 % of the MMA rate at c2;
+// 1.2x faster with the softmax arithmetic removed).  Here the S of tile k+1 is
+// ready when the softmax of tile k ends: the period per tile is max(softmax,
+// MMA) instead of their sum.
 //
-// Warps (10): 0 TMA producer, 1 TMEM owner + MMA issuer (whole warp, elected
-// lane issues), 2..5 softmax set 0, 6..9 softmax set 1; softmax thread = one
-// query row, all 128 keys of its set's key tile in registers.
-// TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256,384), O_1 [384,512);
-// P_X overwrites the first 64 columns of S_X.  Q stays in shared memory (SS QK).
-// Issue order:  QK_0(t0) QK_1(t1) PV_0(t0) QK_0(t2) PV_1(t1) QK_1(t3) ...
+// Warps (10): 0 TMA producer (Q once per item; K/V rings of 128-key tiles, two
+// 64-row segment loads each -- unchanged from v7), 1 TMEM owner + MMA issuer,
+// 2..5 softmax set 0, 6..9 softmax set 1 (thread = one query row, the 64 keys
+// of its set's segment in registers).
+// TMEM (512 columns): O_0 [0,128), O_1 [128,256); S_{X,b} = 256 + 128 X + 64 b
+// (b = tile parity), P_{X,b} overwrites its first 32 columns (64 bf16 keys).
+// MMA order per needed tile k: QK_0(k), QK_1(k), then PV_0(k-1), PV_1(k-1);
+// QK_X(k) overwrites P_X(k-2), whose PV was issued one tile earlier.
+// The two sets cover disjoint keys; their states merge exactly at the end
+// (split-KV identity), as in v7.
 #pragma once
-#include "attn_sm100_v5.cuh"
+#include "attn_sm100_v7.cuh"
 
 namespace lf {
 
 template <int D>
-struct AttnCfg7 {
+struct AttnCfg8 {
   static constexpr int BM = 128;
   static constexpr int BN = 128;
   static constexpr int ATOMS = D / 64;
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int SEG_BYTES = 64 * 128;
-#ifndef LF_V7_KST
-#define LF_V7_KST 2
+#ifndef LF_V8_KST
+#define LF_V8_KST 2
 #endif
-#ifndef LF_V7_VST
-#define LF_V7_VST 3
+#ifndef LF_V8_VST
+#define LF_V8_VST 3
 #endif
-  static constexpr int KST = LF_V7_KST;  // K ring stages
-  static constexpr int VST = LF_V7_VST;  // V ring stages
+  static constexpr int KST = LF_V8_KST;  // K ring stages
+  static constexpr int VST = LF_V8_VST;  // V ring stages
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
@@ -47,28 +50,14 @@ struct AttnCfg7 {
   static constexpr int SMEM = OFF_STAT + 2 * 128 * 8 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
   static constexpr int TMEM_COLS = 512;
-  static constexpr int COL_S = 0;    // + 128 * set
-  static constexpr int COL_O = 256;  // + 128 * set
+  static constexpr int COL_O = 0;    // + 128 * set
+  static constexpr int COL_S = 256;  // + 128 * set + 64 * buffer
 };
-
-// event trace (compile with -DLF_V7_TRACE, run with LF_ATTN_DEBUG=2, LF_ATTN_TRACE_CTA=c):
-// clock64 stamps of CTA c -- softmax [X][k][8] at X*512 (wait start, S ready, stats done,
-// P half 0, P half 1); MMA [kit][4] at 1024 (QK issued, PV wait start, PV issued, K wait
-// start) and K ready at 3072 + kit; items [n][8] at 1536 (producer Q issued, MMA item
-// start, set 0 tail start / O ready / done, set 1 the same).  scripts/trace_v7.py prints it.
-#ifdef LF_V7_TRACE
-#define LF_T7(idx, val) \
-  if ((p.debug & 255) == 2 && (int)blockIdx.x == (p.debug >> 8) && p.trace) p.trace[idx] = (val)
-#else
-#define LF_T7(idx, val) \
-  do {                  \
-  } while (0)
-#endif
 
 template <int D, int POLY>
 __global__ void __launch_bounds__(320, 1)
-    attn_fwd_v7_kernel(const __grid_constant__ AttnParams p, int total_work) {
-  using C = AttnCfg7<D>;
+    attn_fwd_v8_kernel(const __grid_constant__ AttnParams p, int total_work) {
+  using C = AttnCfg8<D>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sQ = smem + C::OFF_Q;
@@ -77,22 +66,19 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* s_full = bars + 2;    // [2] sets
-  uint64_t* p_full = bars + 4;    // [2 sets][2 key halves]
-  uint64_t* o_full = bars + 8;
-  uint64_t* o_empty = bars + 9;
-  uint64_t* k_full = bars + 10;   // [KST <= 4]
-  uint64_t* k_empty = bars + 14;  // [KST]
-  uint64_t* v_full = bars + 18;   // [VST <= 4]
-  uint64_t* v_empty = bars + 22;  // [VST]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
-  int* flag = reinterpret_cast<int*>(bars + 27);
+  uint64_t* s_full = bars + 2;   // [2 sets][2 buffers]
+  uint64_t* p_full = bars + 6;   // [2 sets][2 buffers]
+  uint64_t* o_done = bars + 10;  // [2 sets]: one phase per PV of the set
+  uint64_t* o_full = bars + 12;
+  uint64_t* o_empty = bars + 13;
+  uint64_t* k_full = bars + 14;   // [KST <= 4]
+  uint64_t* k_empty = bars + 18;  // [KST]
+  uint64_t* v_full = bars + 22;   // [VST <= 4]
+  uint64_t* v_empty = bars + 26;  // [VST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
+  int* flag = reinterpret_cast<int*>(bars + 31);
   static_assert(C::KST <= 4 && C::VST <= 4, "barrier slots");
-  // dynamic item schedule (p.sched): the producer warp fetches the next unit
-  // from a global counter when it is ready for its Q and publishes the unit id
-  // through a 4-slot ring to the MMA warp and the 8 softmax warps; null sched:
-  // static round-robin (unit blockIdx.x + k * gridDim.x)
-  constexpr int IR = 4;
+  constexpr int IR = 4;  // dynamic item schedule ring (see v7)
   uint64_t* it_full = bars + 32;   // [IR]
   uint64_t* it_empty = bars + 36;  // [IR]
   int* it_ids = reinterpret_cast<int*>(bars + 40);
@@ -101,7 +87,6 @@ __global__ void __launch_bounds__(320, 1)
     const int w = (int)blockIdx.x + it * (int)gridDim.x;
     return w < total_work ? w : -1;
   };
-  // consumer side: unit of the it-th item of this CTA (-1: done)
   auto take_item = [&](int it) -> int {
     if (!dyn) return next_static(it);
     const int sl = it % IR;
@@ -118,11 +103,12 @@ __global__ void __launch_bounds__(320, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int x = 0; x < 2; ++x) {
+    for (int x = 0; x < 4; ++x) {
       mbar_init(s_full + x, 1);
-      mbar_init(p_full + 2 * x, 128);
-      mbar_init(p_full + 2 * x + 1, 128);
+      mbar_init(p_full + x, 128);
     }
+    mbar_init(o_done + 0, 1);
+    mbar_init(o_done + 1, 1);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 256);
     for (int b = 0; b < C::KST; ++b) {
@@ -146,7 +132,7 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------- TMA producer
+    // ------------------------------------------------------------- TMA producer (v7)
     if (lane == 0) {
       tma_prefetch(&p.tq);
       tma_prefetch(&p.tk);
@@ -175,7 +161,6 @@ __global__ void __launch_bounds__(320, 1)
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
-      if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8, clk64());
       mbar_wait(q_empty, (nq++ & 1) ^ 1);
       if (elect_one()) {
         mbar_expect_tx(q_full, C::Q_BYTES);
@@ -183,7 +168,7 @@ __global__ void __launch_bounds__(320, 1)
           tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, cx.x0, wi.h);
       }
       __syncwarp();
-      TileSegs nx0, nx1;  // the next two entries, loaded ahead (their latency off the loop)
+      TileSegs nx0, nx1;
       if (cx.j0 < cx.j1) nx0 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0);
       if (cx.j0 + 1 < cx.j1) nx1 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0 + 1);
       for (int j = cx.j0; j < cx.j1; ++j) {
@@ -225,7 +210,6 @@ __global__ void __launch_bounds__(320, 1)
         ++kit;
       }
     }
-    // the last CTA past its final fetch resets the schedule for the next launch
     if (dyn && lane == 0) {
       __threadfence();
       if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
@@ -236,12 +220,12 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
-    constexpr uint32_t IDESC_QK = idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t IDESC_QK = idesc_bf16(128, 64, 0, 0);
     constexpr uint32_t IDESC_PV = idesc_bf16(128, D, 0, 1);
     const uint64_t qd = smem_desc_sw128(smem_u32(sQ), 16, 1024);
     const uint64_t kd0 = smem_desc_sw128(smem_u32(sK), 16, 1024);
     const uint64_t vd0 = smem_desc_sw128(smem_u32(sV), C::BN * 128, 1024);
-    uint32_t kit = 0, nq = 0, np[2] = {0, 0}, noe = 0;
+    uint32_t kit = 0, nq = 0, noe = 0;
     for (int it = 0;; ++it) {
       const int w = take_item(it);
       if (w < 0) break;
@@ -249,16 +233,13 @@ __global__ void __launch_bounds__(320, 1)
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
       mbar_wait(q_full, nq & 1);
-      if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8 + 1, clk64());
       ++nq;
-      int pend[2] = {-1, -1};
-      uint32_t pend_kit[2] = {0, 0};
-      bool first_pv[2] = {true, true}, waited_o = false;
+      bool waited_o = false, have_prev = false;
+      uint32_t prev = 0;  // ring index of the tile whose PV is pending
       int k = 0;
-      auto issue_pv = [&](int x) {
-        const uint32_t t = pend_kit[x];
+      // PV of tile t (ring index): both sets, each over its 64-key segment
+      auto issue_pv = [&](uint32_t t, bool first) {
         const int vs = t % C::VST;
-        if (lane == 0 && t < 120) LF_T7(1024 + t * 4 + 1, clk64());
         if (!waited_o) {  // O_0 / O_1 are free once the previous epilogue read them
           mbar_wait(o_empty, (noe & 1) ^ 1);
           ++noe;
@@ -266,25 +247,21 @@ __global__ void __launch_bounds__(320, 1)
         }
         mbar_wait(v_full + vs, (t / C::VST) & 1);
         const uint64_t vd = vd0 + ((uint32_t)(vs * C::KV_BYTES) >> 4);
+        const int b = t & 1;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          mbar_wait(p_full + 2 * x + hh, np[x] & 1);
+        for (int x = 0; x < 2; ++x) {
+          mbar_wait(p_full + 2 * x + b, (t >> 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int kq = 0; kq < C::BN / 32; ++kq) {
-            const int kk = hh * (C::BN / 32) + kq;
-            tc_mma_ts_elect(tmem + C::COL_O + x * 128, tmem + C::COL_S + x * 128 + kk * 8,
-                            vd + ((kk * 16 * 128) >> 4), IDESC_PV,
-                            (!first_pv[x] || kk > 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_ts_elect(tmem + C::COL_O + x * 128, tmem + C::COL_S + x * 128 + b * 64 + kk * 8,
+                            vd + ((uint32_t)(x * C::SEG_BYTES + kk * 16 * 128) >> 4), IDESC_PV,
+                            (!first || kk > 0) ? 1u : 0u);
+          tc_commit_elect(o_done + x);
         }
-        ++np[x];
-        if (lane == 0 && t < 120) LF_T7(1024 + t * 4 + 2, clk64());
         tc_commit_elect(v_empty + vs);
-        first_pv[x] = false;
-        pend[x] = -1;
       };
-      TileSegs nx0, nx1;  // the next two entries, loaded ahead (their latency off the loop)
+      TileSegs nx0, nx1;
       if (cx.j0 < cx.j1) nx0 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0);
       if (cx.j0 + 1 < cx.j1) nx1 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0 + 1);
       for (int j = cx.j0; j < cx.j1; ++j) {
@@ -292,53 +269,44 @@ __global__ void __launch_bounds__(320, 1)
         nx0 = nx1;
         if (j + 2 < cx.j1) nx1 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j + 2);
         if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;
-        const int x = k & 1;
         const int ks = kit % C::KST;
-        if (pend[x] >= 0) issue_pv(x);  // P_x of its previous tile still sits in S_x
-        if (lane == 0 && kit < 120) LF_T7(1024 + kit * 4 + 3, clk64());
+        const int b = kit & 1;
         mbar_wait(k_full + ks, (kit / C::KST) & 1);
-        if (lane == 0 && kit < 120) LF_T7(3072 + kit, clk64());
         tc_fence_after();
         const uint64_t kd = kd0 + ((uint32_t)(ks * C::KV_BYTES) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * (C::BM * 128) + (kk & 3) * 32) >> 4;
-          tc_mma_ss_elect(tmem + C::COL_S + x * 128, qd + off, kd + off, IDESC_QK,
-                          kk > 0 ? 1u : 0u);
+        for (int x = 0; x < 2; ++x) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t qoff = ((kk >> 2) * (C::BM * 128) + (kk & 3) * 32) >> 4;
+            const uint32_t koff = ((kk >> 2) * (C::BN * 128) + x * C::SEG_BYTES + (kk & 3) * 32) >> 4;
+            tc_mma_ss_elect(tmem + C::COL_S + x * 128 + b * 64, qd + qoff, kd + koff, IDESC_QK,
+                            kk > 0 ? 1u : 0u);
+          }
+          tc_commit_elect(s_full + 2 * x + b);
         }
-        tc_commit_elect(s_full + x);
         tc_commit_elect(k_empty + ks);
-        if (lane == 0 && kit < 120) LF_T7(1024 + kit * 4, clk64());
-        pend[x] = 1;
-        pend_kit[x] = kit;
+        if (have_prev) issue_pv(prev, k == 1);
+        have_prev = true;
+        prev = kit;
         ++kit;
         ++k;
       }
-      // drain in issue order: the older pending tile first
-      if (pend[0] >= 0 && pend[1] >= 0) {
-        const int first = pend_kit[0] < pend_kit[1] ? 0 : 1;
-        issue_pv(first);
-        issue_pv(first ^ 1);
-      } else {
-        if (pend[0] >= 0) issue_pv(0);
-        if (pend[1] >= 0) issue_pv(1);
-      }
+      if (have_prev) issue_pv(prev, k == 1);
       tc_commit_elect(q_empty);
       if (k > 0) tc_commit_elect(o_full);
     }
     __syncwarp();
   } else {
     // ------------------------------------------------------------- softmax sets + epilogue
-    const int X = (warp - 2) >> 2;  // softmax set
+    const int X = (warp - 2) >> 2;  // softmax set = key segment of every tile
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t s_col = C::COL_S + X * 128;
     const uint32_t o_col = C::COL_O + X * 128;
     const float c2 = p.scale_log2;
-    uint32_t ns = 0, no = 0, nitem = 0;
-    const bool tr = (warp == 2 || warp == 6) && lane == 0;  // one thread per set
-    for (int it = 0;; ++it, ++nitem) {
+    uint32_t ns = 0, no = 0, npv = 0;  // tiles seen, items finished, PVs of this set so far
+    for (int it = 0;; ++it) {
       const int w = take_item(it);
       if (w < 0) break;
       const WorkItem wi = work_item(p, w);
@@ -351,44 +319,42 @@ __global__ void __launch_bounds__(320, 1)
         lq = lq < 31 ? lq : 31;
       }
       float m_used = -INFINITY, l = 0.f;
-      int k = 0, kx = 0;
+      int k = 0;
+      const uint32_t pv_base = npv;  // o_done phases of this set before this item
       for (int j = cx.j0; j < cx.j1; ++j) {
         const TileSegs ts = tile_segs(p, cx.segs, cx.nseg, cx.Tp, j);
         if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;
-        if (((k++) & 1) != X) continue;  // the other set's key tile
-        const bool row_full =
-            !row_ok || (((ts.m0 & ts.m1) >> lq & 1) && ts.l0 == 64 && ts.l1 == 64);
-        const bool full = __all_sync(0xffffffffu, row_full);
-        if (tr && ns < 60) LF_T7(X * 512 + ns * 8, clk64());
-        mbar_wait(s_full + X, ns & 1);
-        if (tr && ns < 60) LF_T7(X * 512 + ns * 8 + 1, clk64());
+        const int m = X ? ts.m1 : ts.m0;
+        const int len = X ? ts.l1 : ts.l0;
+        const int lim = (!row_ok || ((m >> lq) & 1)) ? len : 0;
+        const bool full = __all_sync(0xffffffffu, lim == 64);
+        const int b = ns & 1;
+        mbar_wait(s_full + 2 * X + b, (ns >> 1) & 1);
         ++ns;
         tc_fence_after();
+        const uint32_t s_col = C::COL_S + X * 128 + b * 64;
         if (p.debug == 1 || p.debug == 3) {  // probe: tensor-core / TMA pipeline without softmax
           tc_fence_before();
-          mbar_arrive(p_full + 2 * X);
-          mbar_arrive(p_full + 2 * X + 1);
+          mbar_arrive(p_full + 2 * X + b);
           l = 1.f;
           m_used = 0.f;
-          ++kx;
+          ++k;
           continue;
         }
-        float v[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(t_row + s_col + 32 * c, v + 32 * c);
+        float v[64];
+        tmem_ld32(t_row + s_col, v);
+        tmem_ld32(t_row + s_col + 32, v + 32);
         tmem_ld_wait();
         if (!full) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) mask_chunk(v + 32 * c, c, ts, lq);
+          for (int e = 0; e < 64; ++e) v[e] = e < lim ? v[e] : -INFINITY;
         }
-        float mx[16];
+        float mx[8];
 #pragma unroll
-        for (int g = 0; g < 16; ++g) {
+        for (int g = 0; g < 8; ++g) {
           const float* u = v + 8 * g;
           mx[g] = fmax3(fmax3(u[0], u[1], u[2]), fmax3(u[3], u[4], u[5]), fmaxf(u[6], u[7]));
         }
-#pragma unroll
-        for (int g = 0; g < 8; ++g) mx[g] = fmaxf(mx[g], mx[g + 8]);
         const float mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]),
                                fmaxf(mx[6], mx[7]));
         // lazy rescale: O_X / l change only when a row max grows by > 2^8
@@ -399,9 +365,13 @@ __global__ void __launch_bounds__(320, 1)
           l *= factor;
           m_used = m_new;
         }
-        if (__any_sync(0xffffffffu, need) && kx > 0) {
-          // O_X holds PV up to this set's previous tile (issued before QK_X of
-          // this tile, so complete once S_X was signalled)
+        if (__any_sync(0xffffffffu, need) && k > 0) {
+          // O_X must hold PV_X of every earlier tile of this item before it is
+          // scaled: wait for the set's PV of tile k-1 (o_done phase pv_base+k-1).
+          // S_X(k) being ready means PV_X(k-2) (issued before QK(k)) is done, so
+          // the barrier is in that phase or the next one: one parity wait is exact.
+          mbar_wait(o_done + X, (pv_base + (uint32_t)k - 1u) & 1);
+          tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < D / 16; ++c) {
             float o[16];
@@ -412,68 +382,59 @@ __global__ void __launch_bounds__(320, 1)
             tmem_st16(t_row + o_col + c * 16, reinterpret_cast<uint32_t*>(o));
           }
         }
-        if (tr && ns - 1 < 60) LF_T7(X * 512 + (ns - 1) * 8 + 2, clk64());
         const float msub = m_used == -INFINITY ? 0.f : m_used * c2;
         const uint64_t c2v = f2pack(c2, c2), nm = f2pack(-msub, -msub);
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
+        for (int e = 0; e < 32; ++e)
           f2unpack(ffma2(f2pack(v[2 * e], v[2 * e + 1]), c2v, nm), v[2 * e], v[2 * e + 1]);
         uint64_t acc[2] = {0ull, 0ull};
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int i2 = 64 * hh + 2 * e;
-            if (POLY > 0 && e % (POLY > 0 ? POLY : 1) == POLY - 1) {
-              exp2_poly2(v[i2], v[i2 + 1]);
-            } else {
-              v[i2] = ex2(v[i2]);
-              v[i2 + 1] = ex2(v[i2 + 1]);
-            }
+        for (int e = 0; e < 32; ++e) {
+          if (POLY > 0 && e % (POLY > 0 ? POLY : 1) == POLY - 1) {
+            exp2_poly2(v[2 * e], v[2 * e + 1]);
+          } else {
+            v[2 * e] = ex2(v[2 * e]);
+            v[2 * e + 1] = ex2(v[2 * e + 1]);
           }
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t pk[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float a = v[64 * hh + 16 * ch + 2 * e], bb = v[64 * hh + 16 * ch + 2 * e + 1];
-              acc[e & 1] = fadd2(acc[e & 1], f2pack(a, bb));
-              pk[e] = pack_bf16(a, bb);
-            }
-            tmem_st8(t_row + s_col + 32 * hh + 8 * ch, pk);
-          }
-          // this key half of P is in TMEM: release its PV
-          tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(p_full + 2 * X + hh);
-          if (tr && ns - 1 < 60) LF_T7(X * 512 + (ns - 1) * 8 + 3 + hh, clk64());
         }
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float a = v[16 * ch + 2 * e], bb = v[16 * ch + 2 * e + 1];
+            acc[e & 1] = fadd2(acc[e & 1], f2pack(a, bb));
+            pk[e] = pack_bf16(a, bb);
+          }
+          tmem_st8(t_row + s_col + 8 * ch, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(p_full + 2 * X + b);
         acc[0] = fadd2(acc[0], acc[1]);
         float a, bb;
         f2unpack(acc[0], a, bb);
         l += a + bb;
-        ++kx;
+        ++k;
       }
+      npv = pv_base + (uint32_t)k;  // one PV (one o_done phase) per published P
       if (cx.T == 0) {
         if (row_ok && X == 0 && p.err) atomicOr(p.err, 1);  // no key at all (callers prevent)
         continue;
       }
-      // ---- merge the two sets' states (split-KV identity) and write out
-      stat[X * 128 + row] = make_float2(m_used, kx > 0 ? l : 0.f);
-      if (tr && nitem < 16) LF_T7(1536 + nitem * 8 + 2 + X * 3, clk64());
+      // ---- merge the two sets' states (split-KV identity) and write out (v7)
+      stat[X * 128 + row] = make_float2(m_used, k > 0 ? l : 0.f);
       if (k > 0) {
         mbar_wait(o_full, no & 1);
         ++no;
         tc_fence_after();
       }
-      if (tr && nitem < 16) LF_T7(1536 + nitem * 8 + 3 + X * 3, clk64());
       asm volatile("bar.sync 1, 256;" ::: "memory");
       const float2 s0 = stat[row], s1 = stat[128 + row];
       const float M = fmaxf(s0.y > 0.f ? s0.x : -INFINITY, s1.y > 0.f ? s1.x : -INFINITY);
       const float f0 = (s0.y > 0.f && s0.x != -INFINITY) ? ex2((s0.x - M) * c2) : 0.f;
       const float f1 = (s1.y > 0.f && s1.x != -INFINITY) ? ex2((s1.x - M) * c2) : 0.f;
       const float L = s0.y * f0 + s1.y * f1;
-      // set X writes columns [X*D/2, (X+1)*D/2) of its rows, 32 at a time
       const long long unit = (long long)wi.slot * wi.nparts + wi.part;
       if (wi.nparts == 1 && row_ok && X == 0 && !(L > 0.f) && p.err) atomicOr(p.err, 1);
       if (k > 0) {
@@ -501,27 +462,26 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(o_empty);  // O_0 / O_1 read: the next item's first PV may overwrite them
-        if (tr && nitem < 16) LF_T7(1536 + nitem * 8 + 4 + X * 3, clk64());
+        mbar_arrive(o_empty);
       }
       if (wi.nparts == 1) {
         if (row_ok && k > 0 && X == 0 && p.lse)
           p.lse[(long long)wi.h * p.Lq + grow] = (M == -INFINITY ? -INFINITY : M * p.scale) + logf(L);
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // stat[] is rewritten by the next item
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         continue;
       }
-      // ---- split-KV: this part's merged, unnormalised O is out; publish (M, L); last part merges
+      // ---- split-KV: publish this part's (M, L); the last part merges (v7)
       if (X == 0) p.part_ml[unit * 128 + row] = make_float2(M, k > 0 ? L : 0.f);
       __threadfence();
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (threadIdx.x == 64) {
         const int old = atomicAdd(p.counters + wi.slot, 1);
         *flag = old == wi.nparts - 1;
-        if (old == wi.nparts - 1) p.counters[wi.slot] = 0;  // reset for the next launch
+        if (old == wi.nparts - 1) p.counters[wi.slot] = 0;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       const bool last = *flag;
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // flag / stat rewritten by the next item
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       if (!last) continue;
       __threadfence();
       const long long base_unit = (long long)wi.slot * wi.nparts;

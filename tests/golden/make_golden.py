@@ -261,6 +261,36 @@ def plan_fixtures():
         json.dump(out, fh, indent=0)
 
 
+def report_fixtures():
+    """The reference CLI's report formats (cli.py:71-78, 125-178, 220-266):
+    a bench CSV (deterministic columns compared), mask-dump PGMs and selection
+    traces, all written by running the reference's own CLI entry points."""
+    import tempfile
+    from chunkattn import cli as ca_cli
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "bench.csv")
+        assert ca_cli.main(["bench", "--seq", "512", "--dim", "64", "--block", "64",
+                            "--densities", "0.5,0.25", "--repeats", "3", "--seed", "5",
+                            "--threads", "1", "--out", out]) == 0
+        with open(out, encoding="utf-8", newline="") as fh:
+            lines = fh.read().split("\r\n")
+        # timing columns (wall_time_*, speedup) and max_abs_err vary run to run: blank them
+        kept = [lines[0], lines[1]]
+        for ln in lines[2:]:
+            if ln:
+                kept.append(",".join(ln.split(",")[:10]))
+        with open(os.path.join(HERE, "report_bench.csv"), "w", encoding="utf-8") as fh:
+            fh.write("\n".join(kept) + "\n")
+        cases = [("global", 0.6, 7), ("per-frame", 0.7, 5)]
+        for mode, sparsity, chunk in cases:
+            pgm = os.path.join(HERE, f"report_mask_{mode}.pgm")
+            tr = os.path.join(HERE, f"report_trace_{mode}.json")
+            assert ca_cli.main(["mask-dump", "--frames", "3", "--tokens", "128", "--block", "64",
+                                "--dim", "32", "--chunks", "7", "--chunk", str(chunk),
+                                "--sparsity", str(sparsity), "--topk", "3", "--mode", mode,
+                                "--seed", "11", "--out", pgm, "--trace", tr]) == 0
+
+
 if __name__ == "__main__":
     pool_fixtures()
     topk_fixtures()
@@ -268,5 +298,6 @@ if __name__ == "__main__":
     attention_fixtures()
     hsa_fixtures()
     framewise_fixtures()
+    report_fixtures()
     for fn in sorted(os.listdir(HERE)):
         print(fn, os.path.getsize(os.path.join(HERE, fn)))
