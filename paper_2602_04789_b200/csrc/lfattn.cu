@@ -11,7 +11,6 @@
 
 #include "attn_sm100_v5.cuh"
 #include "attn_sm100_v7.cuh"
-#include "attn_sm100_v8.cuh"
 #include "cag.cuh"
 #include "pool.cuh"
 #ifndef LF_POOL_DEFAULT
@@ -138,7 +137,6 @@ void init_options() {
     if (const char* e = getenv("LF_QTILE")) g_env_qtile = !strcmp(e, "blocks") ? 1 : *e ? 0 : -1;
     g_opt[LF_OPT_QTILE].store(-1);
     g_opt[LF_OPT_TRACE_CTA].store(env_int("LF_ATTN_TRACE_CTA", 0));
-    g_tile_ver = env_int("LF_TILE_VER", 7);
   });
 }
 
@@ -536,19 +534,8 @@ int launch_tile(AttnParams& p, int heads, int d, int sms, const Scratch* scratch
     attn_fwd_v7_kernel<DD, PV><<<grid, 320, AttnCfg7<DD>::SMEM, S(stream)>>>(p, work);        \
     return check_launch("attn_fwd_v7_kernel");                                               \
   }
-#define LF_V8(DD, PV)                                                                         \
-  if (d == DD && poly == PV) {                                                                \
-    cudaFuncSetAttribute(attn_fwd_v8_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         AttnCfg8<DD>::SMEM);                                                 \
-    attn_fwd_v8_kernel<DD, PV><<<grid, 320, AttnCfg8<DD>::SMEM, S(stream)>>>(p, work);        \
-    return check_launch("attn_fwd_v8_kernel");                                               \
-  }
-  if (g_tile_ver == 8) {
-    LF_V8(128, 0) LF_V8(64, 0) LF_V8(128, 2) LF_V8(128, 3) LF_V8(128, 4) LF_V8(128, 6)
-  }
   LF_V7(128, 0) LF_V7(64, 0) LF_V7(128, 4)
 #undef LF_V7
-#undef LF_V8
   return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v7: d=%d poly=%d not instantiated", d, poly);
 }
 
