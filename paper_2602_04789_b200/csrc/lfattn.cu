@@ -107,8 +107,7 @@ int check_tiling(lf_tiling t, const char* name) {
 // ---- library options (include/lfattn.h LF_OPT_*): the environment is read once,
 // at first use; launch paths read the cached values only
 std::atomic<int> g_opt[LF_OPT_COUNT];
-int g_env_qtile = -1;
-int g_tile_ver = 7;  // tile-kernel generation (LF_TILE_VER=8 during the A/B)  // LF_QTILE from the environment (lf_set_qtile_mode(-1) falls back to it)
+int g_env_qtile = -1;  // LF_QTILE from the environment (lf_set_qtile_mode(-1) falls back to it)
 std::once_flag g_opt_once;
 
 int env_int(const char* name, int dflt) {
