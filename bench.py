@@ -310,16 +310,19 @@ def issued_mma_flops(plan, d):
     ntiles = cnt.shape[1]
     total = 0
     for t in range(ntiles):
-        q0, mid = dv.qtile_rows(qt, mode, 2 * t)
-        q1 = dv.qtile_rows(qt, mode, 2 * t + 1)[1] if 2 * t + 1 < nq else mid
-        qb0 = qt.block_of(q0)
+        if mode == 2:  # paired tiles: plan bits 0, 1 = query tile 2t, bits 2, 3 = 2t + 1
+            ma, mb = 0b0011, 0b1100
+        else:
+            q0, mid = dv.qtile_rows(qt, mode, 2 * t)
+            q1 = dv.qtile_rows(qt, mode, 2 * t + 1)[1] if 2 * t + 1 < nq else mid
+            qb0 = qt.block_of(q0)
 
-        def bits(r0, r1):
-            if r0 >= r1:
-                return 0
-            lo, hi = qt.block_of(r0) - qb0, min(qt.block_of(r1 - 1) - qb0, 31)
-            return ((2 << hi) - 1) & ~((1 << lo) - 1)
-        ma, mb = bits(q0, mid), bits(mid, q1)
+            def bits(r0, r1):
+                if r0 >= r1:
+                    return 0
+                lo, hi = qt.block_of(r0) - qb0, min(qt.block_of(r1 - 1) - qb0, 31)
+                return ((2 << hi) - 1) & ~((1 << lo) - 1)
+            ma, mb = bits(q0, mid), bits(mid, q1)
         for h in range(H):
             n = int(cnt[h, t])
             m = segs[h, t, :n, 2].astype(np.int64)
@@ -550,7 +553,7 @@ def run_ours(args, c):
         def run_attn(s=s, st=st):
             with D.qtile_scope(qmode):
                 D.attention(Q[s], K[s], V[s], qt, st["tiles"], P * n, lk, out=outs[s],
-                            past_tiles=hint)
+                            past_tiles=hint, qperm=st["tiles"].qperm if st["tiles"] else None)
 
         fns = (run_pool, run_sel, run_attn)
         for fn in fns:  # warm (allocates the static buffers the graphs reuse)
@@ -788,9 +791,9 @@ def run_ours(args, c):
             "ms_per_chunk": ms_chunk_r, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": job_config(args, c, s_host, world),
-            "query_tiles": ("block-aligned (2 query blocks)" if (
-                os.environ.get("LF_QTILE", "") == "blocks" or (
-                    not os.environ.get("LF_QTILE") and qmode)) else "128-row"),
+            "query_tiles": {0: "128-row", 1: "block-aligned (2 query blocks)",
+                            2: "2 query blocks paired by selection overlap"}.get(
+                                int(getattr(pl, "qmode", 0) or 0), "128-row"),
             "e2e": {"value": flops_r_step / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                     "ms_per_chunk": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "HsaRollout.commit + prepare/attend (C ABI underneath); H2D, selection, attention and D2H on four streams",

@@ -136,11 +136,12 @@ int lf_plan_tile_rows(void);
  * lf_set_qtile_mode(1) asks for block-aligned query tiles -- two consecutive
  * query blocks per tile, so a ragged framewise tiling (n = 1560, b = 64) never
  * puts 3 query blocks' selections into one tile; plan tile t then covers query
- * tiles 2t and 2t+1 (four query blocks).  0 = 128-row tiles at multiples of
- * 128.  -1 (default): the LF_QTILE environment variable ("blocks" / "rows")
- * when set, else 128-row tiles for lf_plan_tiles / lf_attention(_ex), and an
- * automatic choice inside each lf_hsa_* call (block-aligned when s_i_host
- * gives >= 16 past blocks per query block).  Applies
+ * tiles 2t and 2t+1 (four query blocks).  2 = two query blocks per tile
+ * paired by selection overlap (lf_pair_qblocks; the planner and the attention
+ * take the pairing).  0 = 128-row tiles at multiples of 128.  -1 (default): the
+ * LF_QTILE environment variable ("blocks" / "paired" / "rows") when set, else
+ * 128-row tiles for lf_plan_tiles / lf_attention(_ex), and an automatic choice
+ * inside each lf_hsa_* call (from s_i_host's past blocks per query block).  Applies
  * to tilings with 33..64-row blocks; lf_qtile_mode() returns the mode a tiling
  * gets, lf_plan_tile_count() its number of plan tiles (the `ntiles` of the
  * lf_plan_tiles outputs).  Set it before planning; the planner and the
@@ -170,7 +171,9 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
  *               the fp64 error of any summation order of the reference's dot
  *               products proves the reference selects the same sets
  *               (selection.py:117-175, numerics.py:91-104).
- *   list_blocks / seg_cap / segs / seg_count as lf_plan_tiles.               */
+ *   list_blocks / seg_cap / segs / seg_count as lf_plan_tiles.
+ *   qperm       the query-block pairing when the geometry is 2 (paired query
+ *               tiles, lf_pair_qblocks), else unused (may be NULL).          */
 int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_stride,
                    const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
                    int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
@@ -179,7 +182,23 @@ int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_s
                    int32_t* out_count, int32_t* out_frames, int32_t* out_budget,
                    double* out_margin, lf_tiling q_tiling, lf_tiling k_tiling,
                    int32_t list_blocks, int32_t seg_cap, int32_t* segs, int32_t* seg_count,
-                   void* stream);
+                   int32_t* qperm, void* stream);
+
+/* Query-tile geometry 2: pair each head's query blocks into 128-row tensor-core
+ * tiles by the overlap of their selected past key blocks (mutual-best rounds,
+ * deterministic), so a tile computes fewer key blocks only one half needs.
+ * Regrouping only: each row still attends to exactly its own selection.
+ *   qperm  [H][2 * ceil(nqb / 2)]: query block of half s of query tile t at
+ *          2t + s (-1: none).  Feed it to lf_plan_tiles_paired and
+ *          lf_attention_paired (the geometry must be 2 for both, see
+ *          lf_set_qtile_mode). */
+int lf_pair_qblocks(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                    int32_t cap, int32_t list_blocks, int32_t* qperm, void* stream);
+/* lf_plan_tiles with the geometry-2 pairing (qperm; NULL for geometries 0/1). */
+int lf_plan_tiles_paired(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                         int32_t cap, lf_tiling q_tiling, lf_tiling k_tiling,
+                         int32_t list_blocks, int32_t seg_cap, int32_t* segs,
+                         int32_t* seg_count, const int32_t* qperm, void* stream);
 
 /* Block-sparse flash attention (tcgen05 + TMEM + TMA, bf16 in, fp32 accum).
  * Query tile t of head h attends to its segments plus the dense key range
@@ -233,6 +252,15 @@ int lf_attention_ws(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
                     float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
                     void* scratch, size_t scratch_bytes, void* stream);
 
+/* lf_attention_ws with the geometry-2 pairing (qperm; NULL for geometries 0/1). */
+int lf_attention_paired(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                        const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                        int32_t dense_lo, int32_t dense_hi, float scale, void* out,
+                        int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
+                        float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
+                        void* scratch, size_t scratch_bytes, const int32_t* qperm,
+                        void* stream);
+
 /* One full hot-path call for all heads of one layer at one denoising step of
  * chunk i: compress -> select -> plan tiles -> sparse attention.  Replaces
  * selection.py:196-231 (hsa_attention).  Workspace from lf_hsa_workspace_bytes. */
@@ -278,7 +306,7 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
 #define LF_OPT_ATTN_DEBUG 6   /* LF_ATTN_DEBUG: 1 skip softmax, 2 event trace        */
 #define LF_OPT_ATTN_POLY 7    /* LF_ATTN_POLY: polynomial exp2 on every n-th pair    */
 #define LF_OPT_ATTN_KERNEL 8  /* LF_ATTN_VER (5/7): forced attention kernel, 0 auto  */
-#define LF_OPT_QTILE 9        /* LF_QTILE (blocks|rows) / lf_set_qtile_mode           */
+#define LF_OPT_QTILE 9        /* LF_QTILE (blocks|paired|rows) / lf_set_qtile_mode    */
 #define LF_OPT_TRACE_CTA 10   /* LF_ATTN_TRACE_CTA                                   */
 #define LF_OPT_COUNT 11
 int lf_set_option(int32_t opt, int32_t value); /* LF_ERR_INVALID for an unknown opt */

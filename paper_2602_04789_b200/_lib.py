@@ -27,7 +27,8 @@ LF_KERNEL_AUTO, LF_KERNEL_TILE, LF_KERNEL_PAIR = 0, 3, 5
 # every symbol include/lfattn.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "lf_version", "lf_strerror", "lf_last_error", "lf_pool_blocks", "lf_compress", "lf_select",
-    "lf_select_strided", "lf_select_plan",
+    "lf_select_strided", "lf_select_plan", "lf_pair_qblocks", "lf_plan_tiles_paired",
+    "lf_attention_paired",
     "lf_cag_plan", "lf_plan_tile_rows", "lf_pool_chunk_k", "lf_set_qtile_mode",
     "lf_qtile_mode", "lf_plan_tile_count", "lf_plan_tiles", "lf_attention", "lf_attention_ex",
     "lf_attention_kernel_choice", "lf_hsa_workspace_bytes", "lf_hsa_views",
@@ -80,7 +81,14 @@ _SIGS = {
                            _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "lf_select_plan": ([_P, _P, ctypes.c_int64, _P, ctypes.c_int64, _I, _I, _I, _I, _I, _I, _I,
                         _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, LfTiling, LfTiling, _I, _I, _P,
-                        _P, _P], ctypes.c_int),
+                        _P, _P, _P], ctypes.c_int),
+    "lf_pair_qblocks": ([_P, _P, _I, _I, _I, _I, _P, _P], ctypes.c_int),
+    "lf_plan_tiles_paired": ([_P, _P, _I, _I, _I, LfTiling, LfTiling, _I, _I, _P, _P, _P, _P],
+                             ctypes.c_int),
+    "lf_attention_paired": ([ctypes.POINTER(LfMat), ctypes.POINTER(LfMat),
+                             ctypes.POINTER(LfMat), LfTiling, _P, _P, _I, _I, _I, ctypes.c_float,
+                             _P, _I, ctypes.c_int64, ctypes.c_int64, _P, _P, _I, _I, _P,
+                             ctypes.c_size_t, _P, _P], ctypes.c_int),
     "lf_cag_plan": ([ctypes.c_double, ctypes.c_double, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P,
                      _P, _P, _P, _P], ctypes.c_int),
     "lf_plan_tile_rows": ([], ctypes.c_int),

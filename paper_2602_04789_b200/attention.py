@@ -66,12 +66,14 @@ def sparse_attention_device(qd, kd, vd, bits: np.ndarray, qt: D.TilingSpec, kt: 
     blocks, counts = mask_lists(bits)
     blocks_t = torch.from_numpy(blocks).to(dev)
     counts_t = torch.from_numpy(counts).to(dev)
-    tiles = D.plan_tiles(blocks_t, counts_t, qt, kt, list_blocks=bits.shape[1])
+    qperm = (D.pair_qblocks(blocks_t, counts_t, bits.shape[1]) if D.qtile_mode(qt) == 2
+             else None)
+    tiles = D.plan_tiles(blocks_t, counts_t, qt, kt, list_blocks=bits.shape[1], qperm=qperm)
     qb = C.to_bf16_heads(qd)
     kb = C.to_bf16_heads(kd)
     vb = C.to_bf16_heads(vd)
     out = D.attention(qb, kb, vb, qt, tiles, 0, 0, out_dtype=out_dtype,
-                      scale=1.0 / math.sqrt(d_true))
+                      scale=1.0 / math.sqrt(d_true), qperm=qperm)
     return out[0, :, :d_true]
 
 

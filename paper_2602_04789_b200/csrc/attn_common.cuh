@@ -42,7 +42,9 @@ struct AttnParams {
   CUtensorMap to;    // v5: bf16 output map (box 64 cols x 32 rows), valid when tma_out
   int tma_out;
   int plan_pairs;    // segs are 256-row (pair) plans
-  int qmode;         // query-tile geometry (qtile_rows in common.cuh); 1 implies plan_pairs
+  int qmode;         // query-tile geometry (qtile_rows in common.cuh); 1, 2 imply plan_pairs
+  const int* qperm;  // geometry 2: [H][2 * n_qtiles] query block of each 64-row tile half
+  CUtensorMap tq2;   // q with 64-row boxes (the tile kernel loads a query tile in two halves)
   float* part_o;    // split partials (tile kernel: fp32 [part][128][D]; pair kernel: fp16 O/l)
   float2* part_ml;  // [part][rows] (row max, row sum)
   int* counters;    // [tail], zero between launches
@@ -128,8 +130,15 @@ struct TileCtx {
   const int4* segs;
   uint32_t qm;      // query-block bits of this 128-row tile in its plan (all: 128-row plans)
   int q0;           // first row of the plan tile (qmask bits are relative to its block)
-  int x0, x1;       // this query tile's rows [x0, x1)
+  int x0, x1;       // this query tile's rows [x0, x1) (geometries 0, 1)
+  int gs[2], sz[2]; // tile rows 64 s .. 64 s + sz[s] - 1 are query rows gs[s] .. (all geometries)
+  int pbit;         // geometry 2: plan-tile bit of tile half 0 (half 1: pbit + 1)
 };
+// query row of tile row r (-1 if the row is padding)
+__device__ __forceinline__ int tile_row_global(const TileCtx& c, int r) {
+  const int s = r >> 6, lr = r & 63;
+  return lr < c.sz[s] ? c.gs[s] + lr : -1;
+}
 __device__ __forceinline__ uint32_t tile_qmask(const AttnParams& p, int q0, int x0, int x1) {
   if (x0 >= x1) return 0u;
   const int b0 = p.qt.block_of(q0);
@@ -144,14 +153,33 @@ __device__ __forceinline__ TileCtx tile_ctx(const AttnParams& p, WorkItem wi) {
   TileCtx c;
   const int n_pairs = (p.n_qtiles + 1) >> 1;
   const int wid = p.plan_pairs ? wi.h * n_pairs + (wi.tile >> 1) : wi.h * p.n_qtiles + wi.tile;
-  qtile_rows(p.qt, p.qmode, wi.tile, c.x0, c.x1);
-  if (p.qmode) {
-    int e;
-    qtile_rows(p.qt, 1, wi.tile & ~1, c.q0, e);
+  if (p.qmode == 2) {
+    const int* pr = p.qperm + (size_t)wi.h * 2 * p.n_qtiles + 2 * wi.tile;
+    for (int s = 0; s < 2; ++s) {
+      const int b = pr[s];
+      c.gs[s] = b >= 0 ? p.qt.start(b) : 0;
+      c.sz[s] = b >= 0 ? p.qt.end(b) - p.qt.start(b) : 0;
+    }
+    c.pbit = 2 * (wi.tile & 1);
+    c.x0 = c.gs[0];
+    c.x1 = c.gs[0] + c.sz[0];
+    c.q0 = 0;
+    c.qm = (pr[0] >= 0 ? 1u << c.pbit : 0u) | (pr[1] >= 0 ? 2u << c.pbit : 0u);
   } else {
-    c.q0 = p.plan_pairs ? (wi.tile >> 1) * 256 : wi.tile * 128;
+    qtile_rows(p.qt, p.qmode, wi.tile, c.x0, c.x1);
+    c.gs[0] = c.x0;
+    c.sz[0] = c.x1 - c.x0 < 64 ? c.x1 - c.x0 : 64;
+    c.gs[1] = c.x0 + 64;
+    c.sz[1] = c.x1 - c.x0 > 64 ? c.x1 - c.x0 - 64 : 0;
+    c.pbit = 0;
+    if (p.qmode) {
+      int e;
+      qtile_rows(p.qt, 1, wi.tile & ~1, c.q0, e);
+    } else {
+      c.q0 = p.plan_pairs ? (wi.tile >> 1) * 256 : wi.tile * 128;
+    }
+    c.qm = p.plan_pairs ? tile_qmask(p, c.q0, c.x0, c.x1) : 0xffffffffu;
   }
-  c.qm = p.plan_pairs ? tile_qmask(p, c.q0, c.x0, c.x1) : 0xffffffffu;
   c.nseg = p.seg_count ? p.seg_count[wid] : 0;
   c.segs = p.segs ? p.segs + (size_t)wid * p.seg_cap : nullptr;
   c.Tp = (c.nseg + 1) >> 1;

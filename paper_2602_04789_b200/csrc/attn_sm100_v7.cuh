@@ -177,10 +177,15 @@ __global__ void __launch_bounds__(320, 1)
       if (cx.j1 == cx.j0) continue;
       if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8, clk64());
       mbar_wait(q_empty, (nq++ & 1) ^ 1);
-      if (elect_one()) {
-        mbar_expect_tx(q_full, C::Q_BYTES);
-        for (int a = 0; a < C::ATOMS; ++a)
-          tma_load_3d(&p.tq, q_full, sQ + a * (C::BM * 128), a * 64, cx.x0, wi.h);
+      if (elect_one()) {  // the tile's two 64-row halves (geometry 2: any two query blocks)
+        const int halves = (cx.sz[0] > 0) + (cx.sz[1] > 0);
+        mbar_expect_tx(q_full, halves * (C::Q_BYTES / 2));
+        for (int hs = 0; hs < 2; ++hs) {
+          if (cx.sz[hs] == 0) continue;  // rows never stored: stale shared memory is fine
+          for (int a = 0; a < C::ATOMS; ++a)
+            tma_load_3d(&p.tq2, q_full, sQ + a * (C::BM * 128) + hs * (64 * 128), a * 64,
+                        cx.gs[hs], wi.h);
+        }
       }
       __syncwarp();
       TileSegs nx0, nx1;  // the next two entries, loaded ahead (their latency off the loop)
@@ -343,11 +348,11 @@ __global__ void __launch_bounds__(320, 1)
       if (w < 0) break;
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
-      const int grow = cx.x0 + row;
-      const bool row_ok = grow < cx.x1;
+      const int grow = tile_row_global(cx, row);
+      const bool row_ok = grow >= 0;
       int lq = 0;
       if (row_ok) {
-        lq = p.qt.block_of(grow) - p.qt.block_of(cx.q0);
+        lq = p.qmode == 2 ? cx.pbit + (row >> 6) : p.qt.block_of(grow) - p.qt.block_of(cx.q0);
         lq = lq < 31 ? lq : 31;
       }
       float m_used = -INFINITY, l = 0.f;

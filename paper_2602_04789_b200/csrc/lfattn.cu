@@ -12,6 +12,7 @@
 #include "attn_sm100_v5.cuh"
 #include "attn_sm100_v7.cuh"
 #include "cag.cuh"
+#include "pairing.cuh"
 #include "pool.cuh"
 #ifndef LF_POOL_DEFAULT
 #define LF_POOL_DEFAULT 1
@@ -133,7 +134,8 @@ void init_options() {
     g_opt[LF_OPT_ATTN_POLY].store(env_int("LF_ATTN_POLY", 0));
     const int ver = env_int("LF_ATTN_VER", 0);
     g_opt[LF_OPT_ATTN_KERNEL].store(ver == 5 ? LF_KERNEL_PAIR : ver == 7 ? LF_KERNEL_TILE : 0);
-    if (const char* e = getenv("LF_QTILE")) g_env_qtile = !strcmp(e, "blocks") ? 1 : *e ? 0 : -1;
+    if (const char* e = getenv("LF_QTILE"))
+      g_env_qtile = !strcmp(e, "blocks") ? 1 : !strcmp(e, "paired") ? 2 : *e ? 0 : -1;
     g_opt[LF_OPT_QTILE].store(-1);
     g_opt[LF_OPT_TRACE_CTA].store(env_int("LF_ATTN_TRACE_CTA", 0));
   });
@@ -284,16 +286,19 @@ int max_qblocks_per_tile(lf_tiling qt, int rows = kTileRows) {
 }
 
 // Query-tile geometry (qtile_rows in common.cuh) for a query tiling: 1 =
-// block-aligned tiles (two query blocks each) when requested (lf_set_qtile_mode,
-// else LF_QTILE=blocks) and the blocks are 33..64 rows, else 0 = 128-row tiles.
-// The tile planner and the attention kernel must agree: both read it here.
+// block-aligned tiles (two consecutive query blocks each), 2 = two query blocks
+// paired by selection overlap (pairing.cuh), when requested (lf_set_qtile_mode,
+// else LF_QTILE=blocks|paired, else the lf_hsa_* call's automatic choice) and
+// the blocks are 33..64 rows; else 0 = 128-row tiles.  The tile planner and the
+// attention kernel must agree: both read it here.
 thread_local int g_qmode_scope = -1;  // automatic choice of the lf_hsa_* call in progress
 constexpr int kBlockTilesMinPast = 16;
+constexpr int kPairedMinPast = 100;
 int qmode_for(lf_tiling qt) {
   int req = opt(LF_OPT_QTILE);  // lf_set_qtile_mode
   if (req < 0) req = g_env_qtile;
-  if (req < 0) req = g_qmode_scope > 0 ? 1 : 0;
-  return req && qt.block > 32 && qt.block <= 64 ? 1 : 0;
+  if (req < 0) req = g_qmode_scope > 0 ? g_qmode_scope : 0;
+  return req >= 1 && req <= 2 && qt.block > 32 && qt.block <= 64 ? req : 0;
 }
 // Automatic geometry for one selection step, from the host copy of s_i: the
 // estimated past blocks per query block (budget (1-s_i)*i*f*bpf minus the
@@ -309,7 +314,13 @@ int auto_qmode(double s, int chunk, int f, int n, int b_kv, int topk) {
   const long long cap = (long long)(topk < P ? topk : P) * bpf;
   past = past < cap ? past : cap;
   // every past block selected: all query blocks share one list, nothing to gain
-  return past >= kBlockTilesMinPast && past < (long long)P * bpf ? 1 : 0;
+  if (past < kBlockTilesMinPast || past >= (long long)P * bpf) return 0;
+  // whole retrieved frames (>= 100 past blocks per query block): blocks that
+  // retrieved the same frames select the same keys, so pairing them by
+  // overlap pays for its extra launch (~30 us at 12 heads): attention -17 %
+  // at c5_s50; below it the pairing costs more than it saves (c3 -7 %,
+  // c5_s70 +-0 on the rollout step; profiles/r02/qtile_paired_ab.txt)
+  return past >= kPairedMinPast ? 2 : 1;
 }
 struct QmodeScope {
   int prev;
@@ -501,7 +512,7 @@ int launch_tile(AttnParams& p, int heads, int d, int sms, const Scratch* scratch
   // for dense-like plans (+2 % slower dynamic at c5_dense).  LF_OPT_ATTN_SCHED
   // forces one (profiles/r01/sched_ab.txt).
   const int sched = opt(LF_OPT_ATTN_SCHED);
-  const bool dyn = sched >= 0 ? sched == 1 : p.qmode == 1;
+  const bool dyn = sched >= 0 ? sched == 1 : p.qmode >= 1;
   {
     const int nr = rem > 0 ? rem : 0;
     const size_t need_c = (size_t)(nr + 8) * 4;
@@ -595,7 +606,7 @@ int past_tiles_estimate(const lf_hsa_args* a, const HsaGeom& g) {
 
 struct HsaWs {
   float *q_block, *k_block, *k_frame;
-  int *blocks, *count, *frames, *budget, *seg_count;
+  int *blocks, *count, *frames, *budget, *seg_count, *qperm;
   int4* segs;
   char* scratch;  // attention split-KV scratch (zero-filled with the workspace)
   size_t scratch_bytes;
@@ -619,6 +630,7 @@ HsaWs carve(const HsaGeom& g, void* base) {
   w.budget = reinterpret_cast<int*>(take(16));
   w.segs = reinterpret_cast<int4*>(take((size_t)g.H * g.ntiles * g.seg_cap * 16));
   w.seg_count = reinterpret_cast<int*>(take((size_t)g.H * g.ntiles * 4));
+  w.qperm = reinterpret_cast<int*>(take((size_t)g.H * 2 * ((g.nqb + 1) / 2) * 4));
   w.scratch_bytes = tile_scratch_bytes(g.d, sm_count());
   w.scratch = take(w.scratch_bytes);
   w.bytes = off;
@@ -635,7 +647,7 @@ int lf_version(void) { return 100; }
 int lf_plan_tile_rows(void) { return plan_rows(); }
 void lf_set_qtile_mode(int32_t mode) {
   init_options();
-  g_opt[LF_OPT_QTILE].store(mode < 0 ? -1 : mode ? 1 : 0);
+  g_opt[LF_OPT_QTILE].store(mode < 0 ? -1 : (mode >= 1 && mode <= 2) ? mode : 0);
 }
 
 int lf_set_option(int32_t o, int32_t value) {
@@ -904,6 +916,32 @@ int lf_cag_plan(double s_target, double s_base, int32_t N, int32_t T, int32_t f,
 int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
                   int32_t cap, lf_tiling q_tiling, lf_tiling k_tiling, int32_t list_blocks,
                   int32_t seg_cap, int32_t* segs, int32_t* seg_count, void* stream) {
+  return lf_plan_tiles_paired(blocks, count, heads, nqb, cap, q_tiling, k_tiling, list_blocks,
+                              seg_cap, segs, seg_count, nullptr, stream);
+}
+
+int lf_pair_qblocks(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                    int32_t cap, int32_t list_blocks, int32_t* qperm, void* stream) {
+  if (!qperm || heads < 1 || nqb < 1) return fail(LF_ERR_INVALID, "lf_pair_qblocks: bad args");
+  if (list_blocks > 0 && (!blocks || !count))
+    return fail(LF_ERR_INVALID, "lf_pair_qblocks: null input");
+  const int lb = list_blocks > 0 ? list_blocks : 0;
+  const int words = ((lb + 31) / 32) | 1;  // odd row stride: conflict-free lane-per-row reads
+  const size_t smem = (size_t)nqb * words * 4 + align_up((size_t)nqb * nqb * 2, 4) + nqb * 12 + 4;
+  if (smem > 200 * 1024 || nqb > 1000)
+    return fail(LF_ERR_UNSUPPORTED, "pairing working set too large");
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(pair_qblocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  PairArgs a{blocks, count, nqb, cap, lb, words, qperm};
+  pair_qblocks_kernel<<<heads, kPairThreads, smem, S(stream)>>>(a);
+  return check_launch("pair_qblocks_kernel");
+}
+
+int lf_plan_tiles_paired(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                         int32_t cap, lf_tiling q_tiling, lf_tiling k_tiling,
+                         int32_t list_blocks, int32_t seg_cap, int32_t* segs,
+                         int32_t* seg_count, const int32_t* qperm, void* stream) {
   int rc;
   if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
   if ((rc = check_tiling(k_tiling, "k_tiling"))) return rc;
@@ -922,8 +960,11 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
   int wpc = (200 * 1024) / spw;
   if (wpc < 1) return fail(LF_ERR_UNSUPPORTED, "too many key blocks (%d)", list_blocks);
   wpc = wpc > 4 ? 4 : wpc;
+  if (qmode == 2 && !qperm)
+    return fail(LF_ERR_INVALID, "paired query tiles need the pairing (lf_pair_qblocks)");
   PlanArgs a{blocks, count, heads, nqb, cap, Tiling(q_tiling), Tiling(k_tiling), list_blocks,
-             ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc, rows, qmode};
+             ntiles, seg_cap, reinterpret_cast<int4*>(segs), seg_count, wpc, rows, qmode,
+             qperm};
   if (qmode || opt(LF_OPT_PLAN_WARP) != 1) {  // the warp planner knows 128/256-row tiles only
     if (spw > 48 * 1024)
       cudaFuncSetAttribute(plan_tiles_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, spw);
@@ -946,15 +987,23 @@ int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_s
                    int32_t* out_count, int32_t* out_frames, int32_t* out_budget,
                    double* out_margin, lf_tiling q_tiling, lf_tiling k_tiling,
                    int32_t list_blocks, int32_t seg_cap, int32_t* segs, int32_t* seg_count,
-                   void* stream) {
+                   int32_t* qperm, void* stream) {
   int rc;
+  if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
+  const bool paired = qmode_for(q_tiling) == 2;
+  if (paired && !qperm)
+    return fail(LF_ERR_INVALID, "paired query tiles need a qperm output (lf_pair_qblocks)");
   if ((rc = select_launch(q_block, k_block, kb_head_stride, k_frame, kf_head_stride, heads, nqb,
                           nkb, d, blocks_per_frame, chunk_index, frames_per_chunk, topk_frames,
                           per_frame_mode, s_i_dev, cap, frame_cap, out_blocks, out_count,
                           out_frames, nullptr, nullptr, out_budget, out_margin, stream)))
     return rc;
-  return lf_plan_tiles(out_blocks, out_count, heads, nqb, cap, q_tiling, k_tiling, list_blocks,
-                       seg_cap, segs, seg_count, stream);
+  if (paired && (rc = lf_pair_qblocks(out_blocks, out_count, heads, nqb, cap, list_blocks, qperm,
+                                      stream)))
+    return rc;
+  return lf_plan_tiles_paired(out_blocks, out_count, heads, nqb, cap, q_tiling, k_tiling,
+                              list_blocks, seg_cap, segs, seg_count, paired ? qperm : nullptr,
+                              stream);
 }
 
 int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
@@ -990,6 +1039,19 @@ int lf_attention_ws(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
                     int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
                     float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
                     void* scratch, size_t scratch_bytes, void* stream) {
+  return lf_attention_paired(q, k, v, q_tiling, segs, seg_count, seg_cap, dense_lo, dense_hi,
+                             scale, out, out_dtype, out_row_stride, out_head_stride, lse,
+                             err_flag, kernel, past_tiles_hint, scratch, scratch_bytes, nullptr,
+                             stream);
+}
+
+int lf_attention_paired(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_tiling,
+                        const int32_t* segs, const int32_t* seg_count, int32_t seg_cap,
+                        int32_t dense_lo, int32_t dense_hi, float scale, void* out,
+                        int32_t out_dtype, int64_t out_row_stride, int64_t out_head_stride,
+                        float* lse, int32_t* err_flag, int32_t kernel, int32_t past_tiles_hint,
+                        void* scratch, size_t scratch_bytes, const int32_t* qperm,
+                        void* stream) {
   int rc;
   if ((rc = check_mat(q, "q")) || (rc = check_mat(k, "k")) || (rc = check_mat(v, "v"))) return rc;
   if ((rc = check_tiling(q_tiling, "q_tiling"))) return rc;
@@ -1010,11 +1072,15 @@ int lf_attention_ws(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling
   if (!out) return fail(LF_ERR_INVALID, "null out");
   AttnParams p;
   memset(&p, 0, sizeof(p));
-  if ((rc = make_map(&p.tq, q, 128)) || (rc = make_map(&p.tk, k, 64)) || (rc = make_map(&p.tv, v, 64)))
+  if ((rc = make_map(&p.tq, q, 128)) || (rc = make_map(&p.tq2, q, 64)) ||
+      (rc = make_map(&p.tk, k, 64)) || (rc = make_map(&p.tv, v, 64)))
     return rc;
   p.qt = Tiling(q_tiling);
   p.Lq = q->rows;
   p.qmode = qmode_for(q_tiling);
+  if (p.qmode == 2 && !qperm)
+    return fail(LF_ERR_INVALID, "paired query tiles need the pairing (lf_pair_qblocks)");
+  p.qperm = qperm;
   p.n_qtiles = qtile_count(p.qt, p.qmode);
   p.segs = reinterpret_cast<const int4*>(segs);
   p.seg_count = seg_count;
@@ -1096,15 +1162,16 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
                            a->f, a->topk_frames, a->per_frame_mode, a->s_i_dev, g.cap,
                            g.frame_cap, w.blocks, w.count, w.frames, w.budget, nullptr, g.qt,
                            g.kt, g.list_blocks, g.seg_cap, reinterpret_cast<int32_t*>(w.segs),
-                           w.seg_count, stream)))
+                           w.seg_count, w.qperm, stream)))
     return rc;
   lf_mat kk = a->k, vv = a->v;
   kk.rows = vv.rows = a->chunk_index * a->f * a->n;
-  return lf_attention_ws(&a->q, &kk, &vv, g.qt, reinterpret_cast<const int32_t*>(w.segs),
-                         w.seg_count, g.seg_cap, g.dense_lo, g.dense_hi,
-                         1.0f / sqrtf((float)g.d), a->out, a->out_dtype, a->out_row_stride,
-                         a->out_head_stride, a->lse, a->err_flag, a->attn_kernel,
-                         past_tiles_estimate(a, g), w.scratch, w.scratch_bytes, stream);
+  return lf_attention_paired(&a->q, &kk, &vv, g.qt, reinterpret_cast<const int32_t*>(w.segs),
+                             w.seg_count, g.seg_cap, g.dense_lo, g.dense_hi,
+                             1.0f / sqrtf((float)g.d), a->out, a->out_dtype, a->out_row_stride,
+                             a->out_head_stride, a->lse, a->err_flag, a->attn_kernel,
+                             past_tiles_estimate(a, g), w.scratch, w.scratch_bytes, w.qperm,
+                             stream);
 }
 
 int lf_rowdot(const float* A, int32_t rows, int32_t d, const float* x, double* out, void* stream) {

@@ -34,7 +34,9 @@ struct PlanArgs {
   int* seg_count;
   int warps_per_cta;
   int tile_rows;  // 128 or 256
-  int qmode;      // query-tile geometry (qtile_rows): 0 = 128-row, 1 = block-aligned
+  int qmode;      // query-tile geometry (qtile_rows): 0 = 128-row, 1 = block-aligned,
+                  // 2 = query blocks paired by selection overlap (qperm, pairing.cuh)
+  const int* qperm;  // geometry 2: [H][2 * n_qtiles] query block of each tile half (-1: none)
 };
 
 __global__ void __launch_bounds__(128) plan_tiles_kernel(PlanArgs a) {
@@ -244,6 +246,35 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int w = blockIdx.x;
   const int h = w / a.ntiles, t = w - h * a.ntiles;
+  if (a.qmode == 2) {  // plan tile t = query tiles 2t, 2t+1 = query blocks qperm[4t .. 4t+3]
+    const int nqt = (a.nqb + 1) / 2;
+    const int* pr = a.qperm + (size_t)h * 2 * nqt;
+    int blk[4];
+    for (int j = 0; j < 4; ++j) blk[j] = 4 * t + j < 2 * nqt ? pr[4 * t + j] : -1;
+    int any = 0;
+    for (int j = tid; j < 4; j += 128) any |= blk[j] >= 0 ? a.count[h * a.nqb + blk[j]] : 0;
+    if (!__syncthreads_or(any)) {
+      if (tid == 0) a.seg_count[w] = 0;
+      return;
+    }
+    for (int b = tid; b < a.list_blocks; b += 128) qm[b] = 0u;
+    __syncthreads();
+    unsigned int maskA = 0u, maskB = 0u;
+    for (int j = 0; j < 4; ++j) {
+      if (blk[j] < 0) continue;
+      (j < 2 ? maskA : maskB) |= 1u << j;
+      const int n = a.count[h * a.nqb + blk[j]];
+      const int* lst = a.blocks + ((size_t)h * a.nqb + blk[j]) * a.cap;
+      for (int e = tid; e < n; e += 128) {
+        const int b = lst[e];
+        if (b >= 0 && b < a.list_blocks) atomicOr(&qm[b], 1u << j);
+      }
+    }
+    __syncthreads();
+    emit_plan_segments<4>(qm, a.list_blocks, a.kt, maskA, maskB, true,
+                          a.segs + (size_t)w * a.seg_cap, a.seg_cap, a.seg_count + w, cnt);
+    return;
+  }
   int q0, q1, mid, xe;
   if (a.qmode) {  // plan tile t = query tiles 2t, 2t+1
     qtile_rows(a.qt, 1, 2 * t, q0, mid);

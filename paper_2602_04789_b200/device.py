@@ -31,26 +31,32 @@ _qmode_req = -1
 
 def set_qtile_mode(mode: int) -> None:
     """Query-tile geometry for later plans and attention calls: 1 = block-aligned
-    (two query blocks per tensor-core tile), 0 = 128-row tiles, -1 = automatic
-    (LF_QTILE env when set, else chosen per step by the rollout / pipeline)."""
+    (two consecutive query blocks per tensor-core tile), 2 = two query blocks
+    paired by selection overlap (pair_qblocks), 0 = 128-row tiles, -1 =
+    automatic (LF_QTILE env when set, else chosen per step by the rollout /
+    pipeline)."""
     global _qmode_req
     _qmode_req = -1 if mode < 0 else int(mode)
     L.lib().lf_set_qtile_mode(_qmode_req)
 
 
 BLOCK_TILES_MIN_PAST = 16  # csrc/lfattn.cu kBlockTilesMinPast
+PAIRED_MIN_PAST = 100      # csrc/lfattn.cu kPairedMinPast
 
 
 def auto_qtile_mode(s_host, chunk: int, f: int, bpf: int, topk_frames: int) -> int:
     """Geometry for one step from the host s_i (mirrors auto_qmode in lfattn.cu):
     block-aligned tiles when the estimated past blocks per query block is >= 16
-    and below all past blocks (a fully selected past gives every block one list)."""
+    and below all past blocks (a fully selected past gives every block one list),
+    paired by selection overlap from 100 past blocks on."""
     P = (chunk - 1) * f
     if P <= 0 or s_host is None or not (0.0 <= float(s_host) < 1.0):
         return 0
     cur = f * bpf
     past = min(int((1.0 - float(s_host)) * chunk * cur + 0.5) - cur, min(topk_frames, P) * bpf)
-    return 1 if BLOCK_TILES_MIN_PAST <= past < P * bpf else 0
+    if not BLOCK_TILES_MIN_PAST <= past < P * bpf:
+        return 0
+    return 2 if past >= PAIRED_MIN_PAST else 1
 
 
 @contextlib.contextmanager
@@ -73,7 +79,9 @@ def qtile_mode(qt) -> int:
 
 
 def qtile_rows(qt, mode: int, t: int):
-    """Rows [x0, x1) of query tile t (csrc/common.cuh qtile_rows)."""
+    """Rows [x0, x1) of query tile t (csrc/common.cuh qtile_rows; geometries 0, 1)."""
+    if mode == 2:
+        raise ValueError("paired query tiles have no row range: use the pairing (qperm)")
     if mode:
         nb = qt.count
         x0 = qt.block_start(2 * t)
@@ -236,10 +244,22 @@ class TilePlan:
     segs: torch.Tensor       # [H, ntiles, seg_cap, 4] int32
     seg_count: torch.Tensor  # [H, ntiles] int32
     seg_cap: int
+    qperm: torch.Tensor | None = None  # geometry 2: [H, 2 * n_qtiles] query-block pairing
+
+
+def pair_qblocks(blocks, count, list_blocks: int) -> torch.Tensor:
+    """Geometry-2 pairing of each head's query blocks by selection overlap
+    (lf_pair_qblocks): int32 [H, 2 * ceil(nqb / 2)], -1 = empty half."""
+    lib = L.lib()
+    H, nqb, cap = blocks.shape
+    qperm = torch.empty((H, 2 * ((nqb + 1) // 2)), dtype=torch.int32, device=blocks.device)
+    L.check(lib.lf_pair_qblocks(blocks.data_ptr(), count.data_ptr(), H, nqb, cap,
+                                int(list_blocks), qperm.data_ptr(), L.stream_ptr()))
+    return qperm
 
 
 def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
-               seg_cap: int | None = None) -> TilePlan:
+               seg_cap: int | None = None, qperm: torch.Tensor | None = None) -> TilePlan:
     lib = L.lib()
     H, nqb, cap = blocks.shape
     rows = plan_rows()
@@ -252,9 +272,9 @@ def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
     dev = blocks.device
     segs = torch.empty((H, ntiles, seg_cap, 4), dtype=torch.int32, device=dev)
     seg_count = torch.empty((H, ntiles), dtype=torch.int32, device=dev)
-    L.check(lib.lf_plan_tiles(blocks.data_ptr(), count.data_ptr(), H, nqb, cap, qt.abi(), kt.abi(),
-                              int(list_blocks), int(seg_cap), segs.data_ptr(), seg_count.data_ptr(),
-                              L.stream_ptr()))
+    L.check(lib.lf_plan_tiles_paired(blocks.data_ptr(), count.data_ptr(), H, nqb, cap, qt.abi(),
+                                     kt.abi(), int(list_blocks), int(seg_cap), segs.data_ptr(),
+                                     seg_count.data_ptr(), L.ptr(qperm), L.stream_ptr()))
     return TilePlan(segs, seg_count, seg_cap)
 
 
@@ -289,6 +309,8 @@ def select_plan(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: i
                   + (3 if rows > TILE_ROWS else 0))
     segs = torch.empty((H, ntiles, seg_cap, 4), dtype=torch.int32, device=dev)
     seg_count = torch.empty((H, ntiles), dtype=torch.int32, device=dev)
+    qperm = (torch.empty((H, 2 * ((nqb + 1) // 2)), dtype=torch.int32, device=dev)
+             if qtile_mode(qt) == 2 else None)
     L.check(lib.lf_select_plan(q_block.data_ptr(), k_block.data_ptr(), k_block.stride(0),
                                k_frame.data_ptr() if P > 0 else None,
                                k_frame.stride(0) if P > 0 else 0, H, nqb, nkb, d, int(bpf),
@@ -296,8 +318,10 @@ def select_plan(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: i
                                s_i.data_ptr(), cap, frame_cap, blocks.data_ptr(),
                                count.data_ptr(), frames.data_ptr(), budget.data_ptr(),
                                L.ptr(margin), qt.abi(), kt.abi(), int(list_blocks), int(seg_cap),
-                               segs.data_ptr(), seg_count.data_ptr(), L.stream_ptr()))
-    return (Selections(blocks, count, frames, budget), TilePlan(segs, seg_count, seg_cap), margin)
+                               segs.data_ptr(), seg_count.data_ptr(), L.ptr(qperm),
+                               L.stream_ptr()))
+    return (Selections(blocks, count, frames, budget),
+            TilePlan(segs, seg_count, seg_cap, qperm), margin)
 
 
 def past_tiles_hint(s_host, chunk: int, f: int, bpf: int, topk_frames: int,
@@ -322,7 +346,8 @@ def attention(q, k, v, qt: TilingSpec, tiles: TilePlan | None, dense_lo: int, de
               out: torch.Tensor | None = None, out_dtype=torch.float32, scale: float | None = None,
               lse: torch.Tensor | None = None, err: torch.Tensor | None = None,
               kernel: int = L.LF_KERNEL_AUTO, past_tiles: int = -1,
-              scratch: torch.Tensor | None = None) -> torch.Tensor:
+              scratch: torch.Tensor | None = None,
+              qperm: torch.Tensor | None = None) -> torch.Tensor:
     """Block-sparse flash attention over bf16 [H, L, d] (d in {64, 128}).
 
     kernel / past_tiles: lf_attention_ex's kernel choice and work hint.
@@ -336,14 +361,15 @@ def attention(q, k, v, qt: TilingSpec, tiles: TilePlan | None, dense_lo: int, de
     mq, mk, mv = L.mat(q), L.mat(k), L.mat(v)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
-    L.check(lib.lf_attention_ws(ctypes.byref(mq), ctypes.byref(mk), ctypes.byref(mv), qt.abi(),
-                                tiles.segs.data_ptr() if tiles else None,
-                                tiles.seg_count.data_ptr() if tiles else None,
-                                tiles.seg_cap if tiles else 0, int(dense_lo), int(dense_hi),
-                                float(scale), out.data_ptr(), odt, out.stride(1), out.stride(0),
-                                L.ptr(lse), L.ptr(err), int(kernel), int(past_tiles),
-                                L.ptr(scratch), scratch.numel() if scratch is not None else 0,
-                                L.stream_ptr()))
+    L.check(lib.lf_attention_paired(ctypes.byref(mq), ctypes.byref(mk), ctypes.byref(mv),
+                                    qt.abi(), tiles.segs.data_ptr() if tiles else None,
+                                    tiles.seg_count.data_ptr() if tiles else None,
+                                    tiles.seg_cap if tiles else 0, int(dense_lo), int(dense_hi),
+                                    float(scale), out.data_ptr(), odt, out.stride(1),
+                                    out.stride(0), L.ptr(lse), L.ptr(err), int(kernel),
+                                    int(past_tiles), L.ptr(scratch),
+                                    scratch.numel() if scratch is not None else 0, L.ptr(qperm),
+                                    L.stream_ptr()))
     return out
 
 

@@ -221,7 +221,7 @@ class HsaRollout:
             return D.attention(plan.q, self.kv_k[:, :lk], self.kv_v[:, :lk], plan.qt, plan.tiles,
                                P * lay.n, lk, out=out, out_dtype=self.out_dtype,
                                scale=1.0 / math.sqrt(lay.d), err=self.err, past_tiles=plan.hint,
-                               scratch=self.scratch)
+                               scratch=self.scratch, qperm=plan.tiles.qperm)
 
 
 class StepPlan:
@@ -240,8 +240,8 @@ class StepPlan:
     def device_tensors(self):
         """The CUDA tensors attend() reads (for record_stream)."""
         sel = self.selection
-        out = [self.q, self.q_block, self.tiles.segs, self.tiles.seg_count, sel.blocks, sel.count,
-               sel.frames, sel.budget]
+        out = [self.q, self.q_block, self.tiles.segs, self.tiles.seg_count, self.tiles.qperm,
+               sel.blocks, sel.count, sel.frames, sel.budget]
         return [t for t in out if t is not None and t.is_cuda]
 
 

@@ -243,7 +243,7 @@ def hsa_attention(q, k, v, chunk_index: int, s_i: float, cfg: SelectionConfig,
     qh, kh, vh = C.to_bf16_heads(qd), C.to_bf16_heads(kd), C.to_bf16_heads(vd)
     with _Timer() as t_att:
         out = D.attention(qh, kh, vh, qt, tiles, P * layout.n, ctx, out_dtype=torch.float32,
-                          scale=1.0 / math.sqrt(layout.d))
+                          scale=1.0 / math.sqrt(layout.d), qperm=tiles.qperm)
     count = sel.count[0].cpu().numpy()
     blocks = sel.blocks[0].cpu().numpy()
     budget = sel.budget.cpu().numpy()

@@ -54,3 +54,97 @@ print(f"effective tile-equivalents {eff:.0f}")
 print(f"128-row tiles: {len(aligned)} query tiles, issued {a} (eff/issued {eff / a:.2f})")
 print(f"block-aligned: {len(blockwise)} query tiles, issued {bw} (eff/issued {eff / bw:.2f}), "
       f"{100 * (bw - a) / a:+.1f} %")
+
+# greedy pairing of query blocks by selection overlap (largest shared 64-key
+# segment count first), within the head; unpaired blocks ride alone
+def overlap_pairs():
+    sets = [past[r] for r in range(nqb)]
+    left = set(range(nqb))
+    pairs = []
+    cand = []
+    for a_ in range(nqb):
+        for b_ in range(a_ + 1, nqb):
+            cand.append((int((sets[a_] & sets[b_]).sum()), a_, b_))
+    cand.sort(reverse=True)
+    for ov, a_, b_ in cand:
+        if a_ in left and b_ in left:
+            pairs.append([a_, b_])
+            left.discard(a_)
+            left.discard(b_)
+    pairs += [[r] for r in sorted(left)]
+    return pairs
+
+
+jp = overlap_pairs()
+jw = issued(jp) + len(jp) * kt_cur
+print(f"overlap-paired: {len(jp)} query tiles, issued {jw} (eff/issued {eff / jw:.2f}), "
+      f"{100 * (jw - a) / a:+.1f} % vs 128-row, {100 * (jw - bw) / bw:+.1f} % vs block-aligned")
+
+
+# pairing by sorting query blocks on their retrieved-frame set (the kernel's
+# cheap surrogate for overlap pairing): equal frame sets end up adjacent
+def frame_sort_pairs():
+    keys = []
+    for r in range(nqb):
+        fr = sorted(int(t) for t in sel.frames[r] if t < (i - 1) * f)
+        keys.append((tuple(fr), r))
+    order = [r for _, r in sorted(keys)]
+    return [order[j:j + 2] for j in range(0, len(order), 2)]
+
+
+fp = frame_sort_pairs()
+fw_ = issued(fp) + len(fp) * kt_cur
+print(f"frame-sorted:   {len(fp)} query tiles, issued {fw_} (eff/issued {eff / fw_:.2f}), "
+      f"{100 * (fw_ - bw) / bw:+.1f} % vs block-aligned")
+
+
+def mutual_best_pairs(max_rounds):
+    """The device kernel's mutual-best rounds (pairing.cuh), at most max_rounds."""
+    ov = np.zeros((nqb, nqb), np.int64)
+    for a_ in range(nqb):
+        for b_ in range(nqb):
+            if a_ != b_:
+                ov[a_, b_] = int((past[a_] & past[b_]).sum())
+    mate = [-1] * nqb
+    rounds = 0
+    for _ in range(max_rounds):
+        prop = []
+        for x in range(nqb):
+            best, key = -1, None
+            if mate[x] < 0:
+                for y in range(nqb):
+                    if y == x or mate[y] >= 0:
+                        continue
+                    k2 = (ov[x, y], -abs(x - y), -y)
+                    if key is None or k2 > key:
+                        key, best = k2, y
+            prop.append(best)
+        new = 0
+        for x in range(nqb):
+            y = prop[x]
+            if y >= 0 and prop[y] == x:
+                mate[x] = y
+                new += 1
+        rounds += 1
+        if new == 0:
+            break
+    pairs, pend = [], None
+    for x in range(nqb):
+        y = mate[x]
+        if y >= 0:
+            if x < y:
+                pairs.append([x, y])
+        elif pend is None:
+            pend = x
+        else:
+            pairs.append([pend, x])
+            pend = None
+    if pend is not None:
+        pairs.append([pend])
+    return pairs, rounds
+
+
+for R in (2, 4, 8, 100):
+    mp, rr = mutual_best_pairs(R)
+    mw = issued(mp) + len(mp) * kt_cur
+    print(f"mutual-best <= {R} rounds (ran {rr}): issued {mw}, {100 * (mw - bw) / bw:+.1f} % vs block-aligned")
