@@ -9,10 +9,11 @@ def test_auto_choice_at_the_bench_configs():
     # c2 / c5_s85: (almost) no past blocks -> 128-row tiles
     assert D.auto_qtile_mode(6 / 7, 7, 3, bpf, 6) == 0
     assert D.auto_qtile_mode(0.85, 7, 3, bpf, 6) == 0
-    # c3 (chunk 14, 25 past blocks per query block), c5_s50 / c5_s70 -> block-aligned
+    # c3 (chunk 14, 25 past blocks per query block), c5_s70 (83) -> block-aligned
     assert D.auto_qtile_mode(0.904632706980882, 14, 3, bpf, 6) == 1
-    assert D.auto_qtile_mode(0.5, 7, 3, bpf, 6) == 1
     assert D.auto_qtile_mode(0.7, 7, 3, bpf, 6) == 1
+    # c5_s50: whole retrieved frames (150 past blocks) -> paired by selection overlap
+    assert D.auto_qtile_mode(0.5, 7, 3, bpf, 6) == 2
     # c5_dense: every past block selected (topk covers all 18 frames) -> 128-row tiles
     assert D.auto_qtile_mode(0.0, 7, 3, bpf, 18) == 0
     # chunk 1 and unknown s_i
@@ -43,6 +44,9 @@ def test_c_abi_geometry_queries_on_host():
         assert lib.lf_qtile_mode(qt.abi()) == 1
         assert lib.lf_plan_tile_count(qt.abi()) == -(-qt.count // 4)  # 75 blocks -> 19
         assert lib.lf_qtile_mode(D.TilingSpec(1024, 1024, 128).abi()) == 0
+        lib.lf_set_qtile_mode(2)  # paired: same tile counts as block-aligned
+        assert lib.lf_qtile_mode(qt.abi()) == 2
+        assert lib.lf_plan_tile_count(qt.abi()) == -(-qt.count // 4)
         lib.lf_set_qtile_mode(0)
         assert lib.lf_qtile_mode(qt.abi()) == 0
         assert lib.lf_plan_tile_count(qt.abi()) == -(-qt.total // 256)
