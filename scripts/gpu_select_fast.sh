@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_select_plan.py tests/test_gpu_parity.py tests/test_gpu_rollout.py -m gpu -x -q 2>&1 | tail -3
+for c in c2 c3 c5_s50 c5_s70; do for ex in 1 0; do
+  if [ $ex = 1 ]; then export LF_SELECT_EXACT=1; else unset LF_SELECT_EXACT; fi; timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/sx.json 2>/dev/null
+  python -c "import json;d=json.load(open('gpurun_out/sx.json'));s=d['roofline_select'];print('$c exact=$ex headline', round(d['value']), 'stateless', round(d['stateless']['value']), 'selplan us', round(s['select_plan_ms_per_call']*1e3,1), 'stage', round(s['frac'],3))" 2>&1 | tail -1
+done; done
