@@ -382,6 +382,38 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(t_row + s_col + 32 * c, v + 32 * c);
         tmem_ld_wait();
+        if (p.debug >= 4) {  // probes: 4 = S load only, 5 = + row max, 6 = + exps, 7 = + P store
+          float mxx = v[0], sum = 0.f;
+          if (p.debug >= 5) {
+#pragma unroll
+            for (int e = 1; e < 128; ++e) mxx = fmaxf(mxx, v[e]);
+          }
+          if (p.debug >= 6) {
+#pragma unroll
+            for (int e = 0; e < 128; ++e) {
+              v[e] = ex2((v[e] - mxx) * c2);
+              sum += v[e];
+            }
+          }
+          if (p.debug >= 7) {
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              uint32_t pk[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) pk[e] = pack_bf16(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]);
+              tmem_st8(t_row + s_col + 8 * ch, pk);
+            }
+            tmem_st_wait();
+          }
+          if ((mxx == 12345.f || sum == 12345.f) && p.err) atomicOr(p.err, 2);  // keep it alive
+          tc_fence_before();
+          mbar_arrive(p_full + 2 * X);
+          mbar_arrive(p_full + 2 * X + 1);
+          l = 1.f;
+          m_used = 0.f;
+          ++kx;
+          continue;
+        }
         if (!full) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) mask_chunk(v + 32 * c, c, ts, lq);
