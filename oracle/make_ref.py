@@ -11,7 +11,9 @@ to the GPU box, where /root/reference does not exist.  Users:
     package's backends, and the reference CPU rollout they are compared with;
   * bench.py's reference arm -- times the real ``hsa_attention`` at the
     aligned n = 1536 shape beside the framewise port (n = 1560 is rejected by
-    the reference itself, selection.py:88-92).
+    the reference itself, selection.py:88-92);
+  * tests/test_gpu_reference_suite.py -- the reference's own test suite
+    (staged to ``oracle/_ref/tests/``) run against this package.
 
 Never imported by ``paper_2602_04789_b200/``.
 
@@ -29,14 +31,25 @@ SRC = "/root/reference/pkg/src/chunkattn"
 DST = os.path.join(HERE, "_ref", "chunkattn")
 
 
+TESTS_SRC = "/root/reference/pkg/tests"
+TESTS_DST = os.path.join(HERE, "_ref", "tests")
+
+
 def stage(src: str = SRC, dst: str = DST) -> str | None:
-    """Copy the reference package; returns the _ref directory (None if no source)."""
+    """Copy the reference package and its test suite (tests/test_gpu_reference_suite.py
+    runs that suite against this package); returns the _ref directory (None if no
+    source)."""
     if not os.path.isdir(src):
         return os.path.dirname(dst) if os.path.isdir(dst) else None
     os.makedirs(dst, exist_ok=True)
     for name in sorted(os.listdir(src)):
         if name.endswith(".py"):
             shutil.copyfile(os.path.join(src, name), os.path.join(dst, name))
+    if os.path.isdir(TESTS_SRC):
+        os.makedirs(TESTS_DST, exist_ok=True)
+        for name in sorted(os.listdir(TESTS_SRC)):
+            if name.endswith(".py"):
+                shutil.copyfile(os.path.join(TESTS_SRC, name), os.path.join(TESTS_DST, name))
     with open(os.path.join(os.path.dirname(dst), "SOURCE"), "w") as fh:
         fh.write(f"{src}\n")
     return os.path.dirname(dst)
