@@ -364,6 +364,11 @@ __global__ void __launch_bounds__(320, 1)
         const bool row_full =
             !row_ok || (((ts.m0 & ts.m1) >> lq & 1) && ts.l0 == 64 && ts.l1 == 64);
         const bool full = __all_sync(0xffffffffu, row_full);
+        // key halves (segments) some row of this warp attends to: a masked half
+        // gets P = 0 without its exponentials -- the MUFU work is what bounds
+        // the tile, and on mixed sparse tiles whole warps are masked
+        const bool need0 = full || __any_sync(0xffffffffu, row_ok && ((ts.m0 >> lq) & 1) && ts.l0 > 0);
+        const bool need1 = full || __any_sync(0xffffffffu, row_ok && ((ts.m1 >> lq) & 1) && ts.l1 > 0);
         if (tr && ns < 60) LF_T7(X * 512 + ns * 8, clk64());
         mbar_wait(s_full + X, ns & 1);
         if (tr && ns < 60) LF_T7(X * 512 + ns * 8 + 1, clk64());
@@ -382,38 +387,6 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(t_row + s_col + 32 * c, v + 32 * c);
         tmem_ld_wait();
-        if (p.debug >= 4) {  // probes: 4 = S load only, 5 = + row max, 6 = + exps, 7 = + P store
-          float mxx = v[0], sum = 0.f;
-          if (p.debug >= 5) {
-#pragma unroll
-            for (int e = 1; e < 128; ++e) mxx = fmaxf(mxx, v[e]);
-          }
-          if (p.debug >= 6) {
-#pragma unroll
-            for (int e = 0; e < 128; ++e) {
-              v[e] = ex2((v[e] - mxx) * c2);
-              sum += v[e];
-            }
-          }
-          if (p.debug >= 7) {
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-              uint32_t pk[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) pk[e] = pack_bf16(v[16 * ch + 2 * e], v[16 * ch + 2 * e + 1]);
-              tmem_st8(t_row + s_col + 8 * ch, pk);
-            }
-            tmem_st_wait();
-          }
-          if ((mxx == 12345.f || sum == 12345.f) && p.err) atomicOr(p.err, 2);  // keep it alive
-          tc_fence_before();
-          mbar_arrive(p_full + 2 * X);
-          mbar_arrive(p_full + 2 * X + 1);
-          l = 1.f;
-          m_used = 0.f;
-          ++kx;
-          continue;
-        }
         if (!full) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) mask_chunk(v + 32 * c, c, ts, lq);
@@ -458,6 +431,15 @@ __global__ void __launch_bounds__(320, 1)
         uint64_t acc[2] = {0ull, 0ull};
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
+          if (!(hh ? need1 : need0)) {  // masked half for every row of the warp: P = 0
+            const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) tmem_st8(t_row + s_col + 32 * hh + 8 * ch, z);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(p_full + 2 * X + hh);
+            continue;
+          }
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const int i2 = 64 * hh + 2 * e;
