@@ -620,11 +620,19 @@ def run_ours(args, c):
         if world > 1:
             dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(reps)] \
+            if os.environ.get("LF_BENCH_TRACE") else None
         a.record()
-        for _ in range(reps):
+        for r in range(reps):
             fn()
+            if marks:
+                marks[r].record()
         b.record()
         torch.cuda.synchronize()
+        if marks:
+            per = [a.elapsed_time(marks[0])] + [marks[r - 1].elapsed_time(marks[r])
+                                                for r in range(1, reps)]
+            sys.stderr.write("timed: " + " ".join(f"{x:.2f}" for x in per) + "\n")
         tt = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
