@@ -13,6 +13,9 @@ memory by the selection kernel.
 
     python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
 
+LF_BENCH_TRACE=1 prints the per-iteration device times of the timed legs to
+stderr (diagnosing outliers, e.g. of the PCIe-bound e2e leg).
+
 Multi-GPU (torchrun, one rank per GPU): heads are sharded when H % N == 0 and
 the per-head outputs are all-gathered over NCCL (strong scaling); otherwise
 every rank runs an independent video (replicas, weak scaling, no collective).

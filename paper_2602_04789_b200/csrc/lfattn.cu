@@ -922,9 +922,8 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
 
 int lf_pair_qblocks(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
                     int32_t cap, int32_t list_blocks, int32_t* qperm, void* stream) {
-  if (!qperm || heads < 1 || nqb < 1) return fail(LF_ERR_INVALID, "lf_pair_qblocks: bad args");
-  if (list_blocks > 0 && (!blocks || !count))
-    return fail(LF_ERR_INVALID, "lf_pair_qblocks: null input");
+  if (!qperm || !blocks || !count || heads < 1 || nqb < 1 || cap < 1)
+    return fail(LF_ERR_INVALID, "lf_pair_qblocks: bad args");
   const int lb = list_blocks > 0 ? list_blocks : 0;
   const int words = ((lb + 31) / 32) | 1;  // odd row stride: conflict-free lane-per-row reads
   const size_t smem = (size_t)nqb * words * 4 + align_up((size_t)nqb * nqb * 2, 4) + nqb * 12 + 4;
