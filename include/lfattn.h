@@ -75,7 +75,10 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
                 int32_t blocks_per_frame, int32_t past_frames, float* q_block, float* k_block,
                 float* k_frame, void* stream);
 
-/* Hierarchical selection for every (head, query block), one warp each:
+/* Hierarchical selection for every (head, query block), one 128-thread CTA each
+ * (scores screened in fp32 with rigorous bounds, exact fp64 wherever the bounds
+ * do not decide a top-k and for every returned score; paper_2602_04789_b200/
+ * csrc/select.cuh):
  * frame scores (selection.py:117-122), top-k frames (:125-134,
  * numerics.py:91-104), block top-budget inside the retrieved past frames
  * (:137-175, global or per-frame mode), budget from s_i on device
@@ -302,7 +305,8 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
 #define LF_OPT_ATTN_SCHED 3   /* LF_ATTN_DYNAMIC=1 / LF_ATTN_STATIC=1: 1 dynamic, 0
                                  round-robin, -1 auto (dynamic on block-aligned)    */
 #define LF_OPT_PLAN_WARP 4    /* LF_PLAN_WARP: 1 = warp-per-tile planner             */
-#define LF_OPT_SELECT_WARP 5  /* LF_SELECT_WARP: 1 = warp-per-query-block selection  */
+#define LF_OPT_SELECT_EXACT 5 /* LF_SELECT_EXACT: 1 = exact fp64 scores for every
+                                 list (no fp32 screening)                          */
 #define LF_OPT_ATTN_DEBUG 6   /* LF_ATTN_DEBUG: 1 skip softmax, 2 event trace        */
 #define LF_OPT_ATTN_POLY 7    /* LF_ATTN_POLY: polynomial exp2 on every n-th pair    */
 #define LF_OPT_ATTN_KERNEL 8  /* LF_ATTN_VER (5/7): forced attention kernel, 0 auto  */
@@ -314,6 +318,12 @@ int lf_get_option(int32_t opt);                /* -2 for an unknown opt         
 
 /* Helpers for the per-row drop-in functions. */
 /* out[r] = <A[r,:], x> in fp64 (compensated), A fp32 [rows][d].  frame_scores. */
+/* Screened-selection statistics (device-wide, all launches since the last
+ * reset): out4[0] frame lists, out4[1] block lists whose fp32 screen did not
+ * decide the top-k; out4[2] / out4[3] of those, the ones completed by exact
+ * scores of their ambiguous items only (the rest were recomputed whole).
+ * Synchronous (device copy). */
+int lf_select_fallbacks(uint64_t* out4, int32_t reset);
 int lf_rowdot(const float* A, int32_t rows, int32_t d, const float* x, double* out, void* stream);
 /* Stable top-k (ties -> lower index) of fp64 scores; numerics.py:91-104. */
 int lf_topk(const double* scores, int32_t n, int32_t k, int32_t* out_idx, void* stream);

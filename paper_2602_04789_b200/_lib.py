@@ -32,14 +32,14 @@ EXPORTS = (
     "lf_cag_plan", "lf_plan_tile_rows", "lf_pool_chunk_k", "lf_set_qtile_mode",
     "lf_qtile_mode", "lf_plan_tile_count", "lf_plan_tiles", "lf_attention", "lf_attention_ex",
     "lf_attention_kernel_choice", "lf_hsa_workspace_bytes", "lf_hsa_views",
-    "lf_hsa_forward", "lf_rowdot", "lf_topk", "lf_attention_ws", "lf_attention_scratch_bytes",
+    "lf_hsa_forward", "lf_select_fallbacks", "lf_rowdot", "lf_topk", "lf_attention_ws", "lf_attention_scratch_bytes",
     "lf_set_option", "lf_get_option",
 )
 
 # library options (include/lfattn.h LF_OPT_*)
 OPTIONS = {
     "pool_cfg": 0, "pool_no_tma": 1, "attn_split": 2, "attn_sched": 3, "plan_warp": 4,
-    "select_warp": 5, "attn_debug": 6, "attn_poly": 7, "attn_kernel": 8, "qtile": 9,
+    "select_exact": 5, "attn_debug": 6, "attn_poly": 7, "attn_kernel": 8, "qtile": 9,
     "trace_cta": 10,
 }
 
@@ -115,6 +115,7 @@ _SIGS = {
     "lf_hsa_views": ([ctypes.POINTER(LfHsaArgs), _P] + [ctypes.POINTER(_P)] * 7 +
                      [ctypes.POINTER(_I), ctypes.POINTER(_I)], ctypes.c_int),
     "lf_hsa_forward": ([ctypes.POINTER(LfHsaArgs), _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "lf_select_fallbacks": ([_P, _I], ctypes.c_int),
     "lf_rowdot": ([_P, _I, _I, _P, _P, _P], ctypes.c_int),
     "lf_topk": ([_P, _I, _I, _P, _P], ctypes.c_int),
 }

@@ -129,7 +129,7 @@ void init_options() {
     g_opt[LF_OPT_ATTN_SPLIT].store(env_int("LF_ATTN_SPLIT", 0));
     g_opt[LF_OPT_ATTN_SCHED].store(getenv("LF_ATTN_DYNAMIC") ? 1 : getenv("LF_ATTN_STATIC") ? 0 : -1);
     g_opt[LF_OPT_PLAN_WARP].store(getenv("LF_PLAN_WARP") ? 1 : 0);
-    g_opt[LF_OPT_SELECT_WARP].store(getenv("LF_SELECT_WARP") ? 1 : 0);
+    g_opt[LF_OPT_SELECT_EXACT].store(getenv("LF_SELECT_EXACT") ? 1 : 0);
     g_opt[LF_OPT_ATTN_DEBUG].store(env_int("LF_ATTN_DEBUG", 0));
     g_opt[LF_OPT_ATTN_POLY].store(env_int("LF_ATTN_POLY", 0));
     const int ver = env_int("LF_ATTN_VER", 0);
@@ -823,12 +823,6 @@ int lf_pool_chunk_k(const lf_mat* k, lf_tiling k_tiling, int32_t blocks_per_fram
   return check_launch("pool_frames_tma_kernel");
 }
 
-static int select_smem_per_warp(int d, int P, int frame_cap, int max_cand) {
-  size_t b = align_up((size_t)d * 4, 16) + (size_t)P * 8 + (size_t)((frame_cap + 1) & ~1) * 4 +
-             (size_t)max_cand * 8;
-  return (int)align_up(b, 16);
-}
-
 static int select_launch(const float* q_block, const float* k_block, int64_t kb_head_stride,
                          const float* k_frame, int64_t kf_head_stride, int32_t heads, int32_t nqb,
                          int32_t nkb, int32_t d, int32_t blocks_per_frame, int32_t chunk_index,
@@ -847,29 +841,18 @@ static int select_launch(const float* q_block, const float* k_block, int64_t kb_
   if (frame_cap < (kf > 0 ? kf : 1)) return fail(LF_ERR_INVALID, "frame_cap too small");
   if (cap < kf * blocks_per_frame) return fail(LF_ERR_INVALID, "cap too small");
   const int max_cand = kf * blocks_per_frame;
-  const int spw = select_smem_per_warp(d, P, frame_cap, max_cand);
-  int wpc = (200 * 1024) / spw;
-  if (wpc < 1) return fail(LF_ERR_UNSUPPORTED, "selection working set too large");
-  wpc = wpc > 4 ? 4 : wpc;
+  const SelLayout lay(d, P, frame_cap, max_cand);
+  if (lay.bytes > 200 * 1024) return fail(LF_ERR_UNSUPPORTED, "selection working set too large");
   SelArgs a{q_block, k_block, k_frame, heads, nqb, nkb, d, blocks_per_frame, chunk_index,
             frames_per_chunk, topk_frames, per_frame_mode ? 1 : 0, s_i_dev, cap, frame_cap,
-            out_blocks, out_count, out_frames, out_scores, out_fscores, out_budget, wpc, spw,
-            max_cand, (long long)kb_head_stride, (long long)kf_head_stride, out_margin};
-  // one 4-warp CTA per (head, query block); its working set adds the flags
-  const int cta_smem = spw + (int)align_up((size_t)(P > max_cand ? P : max_cand), 16);
-  if (out_margin || (opt(LF_OPT_SELECT_WARP) != 1 && cta_smem <= 200 * 1024)) {
-    if (cta_smem > 200 * 1024) return fail(LF_ERR_UNSUPPORTED, "selection working set too large");
-    if (cta_smem > 48 * 1024)
-      cudaFuncSetAttribute(select_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cta_smem);
-    select_cta_kernel<<<heads * nqb, 128, cta_smem, S(stream)>>>(a);
-    return check_launch("select_cta_kernel");
-  }
-  const int smem = wpc * spw;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int warps = heads * nqb;
-  select_kernel<<<(warps + wpc - 1) / wpc, 32 * wpc, smem, S(stream)>>>(a);
-  return check_launch("select_kernel");
+            out_blocks, out_count, out_frames, out_scores, out_fscores, out_budget, max_cand,
+            (long long)kb_head_stride, (long long)kf_head_stride, out_margin,
+            opt(LF_OPT_SELECT_EXACT) == 1 ? 1 : 0, screen_gamma(d)};
+  // one 4-warp CTA per (head, query block)
+  if (lay.bytes > 48 * 1024)
+    cudaFuncSetAttribute(select_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.bytes);
+  select_screen_kernel<<<heads * nqb, kSelThreads, lay.bytes, S(stream)>>>(a);
+  return check_launch("select_screen_kernel");
 }
 
 int lf_select_strided(const float* q_block, const float* k_block, int64_t kb_head_stride,
@@ -1173,10 +1156,28 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
                              stream);
 }
 
+int lf_select_fallbacks(uint64_t* out4, int32_t reset) {
+  if (!out4) return fail(LF_ERR_INVALID, "lf_select_fallbacks: null");
+  unsigned long long v[4];
+  if (cudaMemcpyFromSymbol(v, g_sel_fallbacks, sizeof v) != cudaSuccess)
+    return fail(LF_ERR_CUDA, "lf_select_fallbacks: read");
+  for (int i = 0; i < 4; ++i) out4[i] = v[i];
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(g_sel_fallbacks, z, sizeof z) != cudaSuccess)
+      return fail(LF_ERR_CUDA, "lf_select_fallbacks: reset");
+  }
+  return LF_OK;
+}
+
 int lf_rowdot(const float* A, int32_t rows, int32_t d, const float* x, double* out, void* stream) {
   if (!A || !x || !out || rows < 0 || d < 1) return fail(LF_ERR_INVALID, "lf_rowdot: bad args");
   if (rows == 0) return LF_OK;
-  rowdot_kernel<<<(rows + 127) / 128, 128, d * 4, S(stream)>>>(A, rows, d, x, out);
+  const int smem = SelLayout::up16(d * 4) + d * 8;
+  if (smem > 200 * 1024) return fail(LF_ERR_UNSUPPORTED, "lf_rowdot: d too large");
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(rowdot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  rowdot_kernel<<<(rows + 31) / 32, kSelThreads, smem, S(stream)>>>(A, rows, d, x, out);
   return check_launch("rowdot_kernel");
 }
 

@@ -211,6 +211,16 @@ def select(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: int, p
     return Selections(blocks, count, frames, budget, scores, fscores)
 
 
+def select_fallbacks(reset: bool = False) -> tuple[int, int, int, int]:
+    """(frame lists, block lists) the fp32 screen did not decide, then (frame,
+    block) lists of those completed from exact scores of their ambiguous items
+    only; summed over every selection launch since the last reset (device-wide
+    counters; synchronous)."""
+    out = (ctypes.c_uint64 * 4)()
+    L.check(L.lib().lf_select_fallbacks(ctypes.cast(out, ctypes.c_void_p), 1 if reset else 0))
+    return tuple(int(v) for v in out)
+
+
 @dataclass
 class CagPlan:
     alpha: torch.Tensor

@@ -1,0 +1,5 @@
+# selection iteration: correctness (selection tests), micro timing, per-phase trace
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_select_plan.py -m gpu -x -q 2>&1 | tail -3
+PYTHONPATH=. timeout 300 python scripts/sel_micro.py
+bash scripts/gpu_sel_trace.sh

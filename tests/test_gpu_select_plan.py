@@ -17,6 +17,8 @@ certificate.
 
 from __future__ import annotations
 
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -37,6 +39,17 @@ def _summaries(seed, H, nqb, nkb, P, d, ties):
     qb = rng.standard_normal((H, nqb, d)).astype(np.float32) * 0.125
     kb = rng.standard_normal((H, nkb, d)).astype(np.float32) * 0.125
     kf = rng.standard_normal((H, max(P, 1), d)).astype(np.float32) * 0.05
+    if ties == "near":
+        # rows one fp32 ulp apart: fp64 scores differ by ~1e-9, far inside the
+        # fp32 screening bound, so the screen cannot decide and the exact
+        # fallback must
+        nudge = lambda x: np.nextafter(x, np.float32(np.inf), dtype=np.float32)
+        kb[:, 1::5] = nudge(kb[:, 0::5][:, : kb[:, 1::5].shape[1]])
+        kb[:, 2::5] = kb[:, 0::5][:, : kb[:, 2::5].shape[1]]
+        if P > 3:
+            kf[:, 1] = nudge(kf[:, 0])
+            kf[:, 2] = kf[:, 0]
+        return qb, kb, kf
     if ties:
         # duplicated rows: exactly equal scores, broken by the lower index
         kb[:, 1::5] = kb[:, 0::5][:, : kb[:, 1::5].shape[1]]
@@ -80,7 +93,7 @@ def test_select_plan_vs_oracle_and_margins(D, case):
     qt = D.TilingSpec(f * n, n if fw else f * n, 64)
     kt = D.TilingSpec(chunk * f * n, n if fw else chunk * f * n, 64)
     P = (chunk - 1) * f
-    qb, kb, kf = _summaries(hash(case) & 0xffff, H, qt.count, kt.count, P, d, ties)
+    qb, kb, kf = _summaries(zlib.crc32(repr(case).encode()) & 0xffff, H, qt.count, kt.count, P, d, ties)
     dev = torch.device("cuda")
     tq, tk, tf = (torch.from_numpy(a).to(dev) for a in (qb, kb, kf))
     with D.qtile_scope(qmode):
@@ -122,6 +135,54 @@ def test_select_plan_vs_oracle_and_margins(D, case):
                 o = kb[h][cand].astype(np.float64) @ qb[h][r].astype(np.float64)
                 gap = _gap(o, np.isin(cand, ids))
                 assert abs(mg[h, r, 1] - gap) <= 1e-12 * max(1.0, np.abs(o).max()), (h, r)
+
+
+SCREEN_CASES = [
+    # the screened hot path (no scores / margins requested) against the oracle;
+    # near-ties and exact ties across the cut go through the exact fallback
+    (3, 3, 1560, 128, 7, 0.7, 6, True, 0, False, "global"),
+    (2, 3, 1560, 128, 7, 0.7, 6, True, 0, "near", "global"),
+    (2, 3, 1560, 128, 14, 0.8, 6, True, 1, True, "global"),
+    (2, 3, 1560, 128, 14, 0.8, 6, True, 1, "near", "global"),
+    (2, 3, 1536, 128, 9, 0.6, 4, False, 0, "near", "per-frame"),
+    (2, 3, 1560, 128, 9, 0.7, 6, True, 0, True, "per-frame"),
+    (2, 2, 256, 64, 3, 0.3, 2, False, 0, "near", "global"),
+    (1, 3, 1560, 128, 22, 0.9, 20, True, 1, "near", "global"),
+]
+
+
+@pytest.mark.parametrize("case", SCREEN_CASES)
+@pytest.mark.parametrize("exact", [0, 1])
+def test_screened_selection_vs_oracle(D, case, exact, lfopt):
+    """Frames and blocks of the screened selection (fp32 scores + bounds,
+    exact re-rank where the bounds do not decide) and of the all-exact option
+    equal the oracle's, including rows one ulp apart and exact duplicates."""
+    lfopt("select_exact", exact)
+    H, f, n, d, chunk, s_i, topk, fw, qmode, ties, mode = case
+    bpf = -(-n // 64)
+    qt = D.TilingSpec(f * n, n if fw else f * n, 64)
+    kt = D.TilingSpec(chunk * f * n, n if fw else chunk * f * n, 64)
+    P = (chunk - 1) * f
+    qb, kb, kf = _summaries(zlib.crc32(repr(case).encode()) & 0xffff, H, qt.count, kt.count, P, d, ties)
+    dev = torch.device("cuda")
+    tq, tk, tf = (torch.from_numpy(a).to(dev) for a in (qb, kb, kf))
+    with D.qtile_scope(qmode):
+        sel, tiles, _ = D.select_plan(tq, tk, tf, bpf, chunk, f, topk, mode == "per-frame", s_i,
+                                      qt, kt, P * bpf)
+    torch.cuda.synchronize()
+    cnt = sel.count.cpu().numpy()
+    blocks = sel.blocks.cpu().numpy()
+    frames = sel.frames.cpu().numpy()
+    past_budget = int(sel.budget.cpu().numpy()[1])
+    for h in range(H):
+        views = O.Views(qb[h], kb[h], kf[h][:P], bpf)
+        for r in range(qt.count):
+            p = O.frame_scores(views, r) if P else np.zeros(0)
+            fr = O.select_frames(p, topk, chunk, f) if P else np.arange(0)
+            past = [int(t) for t in fr if t < P]
+            assert [int(t) for t in frames[h, r] if t >= 0] == past, (h, r)
+            _, ids, _ = O.select_blocks(views, r, fr, past_budget, mode)
+            assert blocks[h, r, :cnt[h, r]].tolist() == [int(x) for x in ids], (h, r)
 
 
 def _fp64_bound(views, r, rows):
