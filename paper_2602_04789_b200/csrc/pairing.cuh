@@ -23,6 +23,31 @@ namespace lf {
 
 constexpr int kPairThreads = 512;
 
+// block-wide exclusive scan of one int per thread (kPairThreads threads);
+// *total = the sum.  Contains barriers.
+__device__ __forceinline__ int cta_exclusive_scan(int v, int* total) {
+  __shared__ int wsum[kPairThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int before = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kPairThreads / 32; ++w) {
+    const int t = wsum[w];
+    before += w < warp ? t : 0;
+    all += t;
+  }
+  __syncthreads();
+  *total = all;
+  return before + incl - v;
+}
+
 struct PairArgs {
   const int* blocks;  // [H][nqb][cap]
   const int* count;   // [H][nqb]
@@ -33,54 +58,45 @@ struct PairArgs {
 __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) {
   extern __shared__ __align__(16) unsigned int pr_smem[];
   const int h = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef LF_PAIR_TRACE
+  long long tr[5];
+  tr[0] = clock64();
+  int rounds = 0;
+#endif
   constexpr int NT = kPairThreads, NW = kPairThreads / 32;
   const int n = a.nqb, W = a.words;
   unsigned int* bits = pr_smem;                                          // [n][W]
   unsigned short* ov = reinterpret_cast<unsigned short*>(bits + n * W);  // [n][n]
   int* prop = reinterpret_cast<int*>(ov + ((n * n + 1) & ~1));           // [n] proposals
   int* mate = prop + n;                                                  // [n] (-1 unpaired)
-  __shared__ int s_new, s_total;
-  int* off = mate + n;  // [n + 1] exclusive prefix of the selection counts
+  __shared__ int s_new;
+  int* cnt = mate + n;  // [n] selection counts
   for (int i = tid; i < n * W; i += NT) bits[i] = 0u;
+  int any = 0;
   for (int i = tid; i < n; i += NT) {
     mate[i] = -1;
     const int c = __ldg(a.count + (size_t)h * n + i);
-    off[i + 1] = c < a.cap ? c : a.cap;
+    cnt[i] = c < a.cap ? c : a.cap;
+    any |= cnt[i];
   }
-  __syncthreads();
-  if (warp == 0) {  // prefix over the counts (n <= 1000)
-    int run = 0;
-    for (int b0 = 0; b0 < n; b0 += 32) {
-      int v = b0 + lane < n ? off[b0 + lane + 1] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-      }
-      if (b0 + lane < n) off[b0 + lane + 1] = run + v;
-      run += __shfl_sync(0xffffffffu, v, 31);
-    }
-    if (lane == 0) {
-      off[0] = 0;
-      s_total = run;
-    }
-  }
-  __syncthreads();
-  // selections -> bitsets: only the valid list entries, all loads in flight together
+  const int total = __syncthreads_or(any);
+  // selections -> bitsets: R threads per row, consecutive lanes on consecutive
+  // rows (different words: no atomic conflicts), R-strided entries per thread
   const int* lst = a.blocks + (size_t)h * n * a.cap;
-  const int total = s_total;
+  const int R = n < NT ? NT / n : 1;
+  for (int task = tid; task < n * R; task += NT) {
+    const int x = task % n, k = task / n, c = cnt[x];
+    const int* row = lst + (size_t)x * a.cap;
 #pragma unroll 4
-  for (int v = tid; v < total; v += NT) {
-    int lo = 0, hi = n - 1;  // row r with off[r] <= v < off[r + 1]
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (off[mid] <= v) lo = mid;
-      else hi = mid - 1;
+    for (int e = k; e < c; e += R) {
+      const int b = __ldg(row + e);
+      if (b >= 0 && b < a.list_blocks) atomicOr(&bits[x * W + (b >> 5)], 1u << (b & 31));
     }
-    const int b = __ldg(lst + (size_t)lo * a.cap + (v - off[lo]));
-    if (b >= 0 && b < a.list_blocks) atomicOr(&bits[lo * W + (b >> 5)], 1u << (b & 31));
   }
   __syncthreads();
+#ifdef LF_PAIR_TRACE
+  tr[1] = clock64();
+#endif
   if (total > 0) {
     // pairwise overlaps (upper triangle, mirrored): a warp per block x, a lane
     // per partner y (rows of odd word stride: conflict-free), over x's non-zero
@@ -108,6 +124,9 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
       }
     }
     __syncthreads();
+#ifdef LF_PAIR_TRACE
+    tr[2] = clock64();
+#endif
     // mutual-best rounds; a warp per proposing block, key = (overlap, nearer, lower index)
     for (int round = 0; round < n; ++round) {
       for (int x = warp; x < n; x += NW) {
@@ -139,34 +158,53 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
         }
       }
       __syncthreads();
+#ifdef LF_PAIR_TRACE
+      ++rounds;
+#endif
       if (s_new == 0) break;
       __syncthreads();
     }
   }
-  if (tid == 0) {  // emit tiles: pairs by their lower block, then leftovers in index order
-    int* out = a.qperm + (size_t)h * 2 * ((n + 1) / 2);
-    int t = 0, pend = -1;
-    for (int x = 0; x < n; ++x) {
-      const int y = mate[x];
-      if (y >= 0) {
-        if (x < y) {
-          out[2 * t] = x;
-          out[2 * t + 1] = y;
-          ++t;
-        }
-      } else if (pend < 0) {
-        pend = x;
-      } else {
-        out[2 * t] = pend;
-        out[2 * t + 1] = x;
-        ++t;
-        pend = -1;
-      }
-    }
-    if (pend >= 0) {
-      out[2 * t] = pend;
-      out[2 * t + 1] = -1;
-    }
+#ifdef LF_PAIR_TRACE
+  tr[3] = clock64();
+#endif
+  // emit tiles in the order of a serial scan over x: a pair at its lower block,
+  // two leftovers (unpaired blocks, index order) at the second of them, an odd
+  // last leftover at the end.  Two block-wide exclusive scans.
+  int* out = a.qperm + (size_t)h * 2 * ((n + 1) / 2);
+  int* ulist = prop;  // [n] unpaired blocks in index order (proposals no longer needed)
+  __syncthreads();
+  const int x0 = 2 * tid, x1 = 2 * tid + 1;  // n <= 1000 < 2 * NT
+  const int m0 = x0 < n ? mate[x0] : 0, m1 = x1 < n ? mate[x1] : 0;
+  const int u0 = x0 < n && m0 < 0, u1 = x1 < n && m1 < 0;
+  int nu;
+  const int ur0 = cta_exclusive_scan(u0 + u1, &nu), ur1 = ur0 + u0;
+  if (u0) ulist[ur0] = x0;
+  if (u1) ulist[ur1] = x1;
+  const int e0 = x0 < n && (m0 > x0 || (u0 && (ur0 & 1)));
+  const int e1 = x1 < n && (m1 > x1 || (u1 && (ur1 & 1)));
+  int ne;
+  const int t0 = cta_exclusive_scan(e0 + e1, &ne), t1 = t0 + e0;
+  __syncthreads();  // ulist complete
+  if (e0) {
+    out[2 * t0] = u0 ? ulist[ur0 - 1] : x0;
+    out[2 * t0 + 1] = u0 ? x0 : m0;
+  }
+  if (e1) {
+    out[2 * t1] = u1 ? ulist[ur1 - 1] : x1;
+    out[2 * t1 + 1] = u1 ? x1 : m1;
+  }
+  if (tid == 0 && (nu & 1)) {
+    out[2 * ne] = ulist[nu - 1];
+    out[2 * ne + 1] = -1;
+  }
+  if (tid == 0) {
+#ifdef LF_PAIR_TRACE
+    tr[4] = clock64();
+    if (h == 0 || h == (int)gridDim.x - 1)
+      printf("pair_trace head %d: bitsets %lld overlaps %lld rounds %lld (%d) emit %lld total %lld\n",
+             h, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], rounds, tr[4] - tr[3], tr[4] - tr[0]);
+#endif
   }
 }
 

@@ -235,6 +235,44 @@ __device__ void emit_plan_segments(const unsigned int* qm, int list_blocks, cons
   }
 }
 
+// qm[b] |= 1 << j for every past key block b in the list of query block qbs[j]
+// (j < nq <= 32, qbs[j] < 0: none).  Counts first, then all list entries in
+// one flattened pass, so the CTA waits for two dependent loads, not 2 * nq.
+// Returns false (CTA-uniform) when the lists are all empty.
+__device__ __forceinline__ bool gather_lists(const PlanArgs& a, int h, const int* qbs, int nq,
+                                             unsigned int* qm, int* off /* [33] shared */) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int b = tid; b < a.list_blocks; b += 128) qm[b] = 0u;
+  if (tid < 32) {
+    int c = 0;
+    if (lane < nq && qbs[lane] >= 0) {
+      c = __ldg(a.count + h * a.nqb + qbs[lane]);
+      c = c < a.cap ? c : a.cap;
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    off[lane + 1] = incl;
+    if (lane == 0) off[0] = 0;
+  }
+  __syncthreads();
+  const int total = off[32];
+  if (total == 0) return false;
+  for (int v = tid; v < total; v += 128) {
+    int j = 0;  // list of entry v: off[j] <= v < off[j + 1]
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1)
+      if (off[j + st] <= v) j += st;
+    const int b = __ldg(a.blocks + ((size_t)h * a.nqb + qbs[j]) * a.cap + (v - off[j]));
+    if (b >= 0 && b < a.list_blocks) atomicOr(&qm[b], 1u << j);
+  }
+  __syncthreads();
+  return true;
+}
+
 // plan_tiles_kernel with one 128-thread CTA per (head, plan tile): the key
 // blocks are split into four contiguous ranges, one per warp; a counting pass
 // gives every warp its output offsets in each class, a second pass writes.
@@ -243,34 +281,22 @@ __device__ void emit_plan_segments(const unsigned int* qm, int list_blocks, cons
 __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   extern __shared__ unsigned int qm[];
   __shared__ int cnt[4][4];  // [warp][class 1..3] (emit_plan_segments)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_qbs[32], s_off[33];
+  const int tid = threadIdx.x;
   const int w = blockIdx.x;
   const int h = w / a.ntiles, t = w - h * a.ntiles;
   if (a.qmode == 2) {  // plan tile t = query tiles 2t, 2t+1 = query blocks qperm[4t .. 4t+3]
     const int nqt = (a.nqb + 1) / 2;
     const int* pr = a.qperm + (size_t)h * 2 * nqt;
-    int blk[4];
-    for (int j = 0; j < 4; ++j) blk[j] = 4 * t + j < 2 * nqt ? pr[4 * t + j] : -1;
-    int any = 0;
-    for (int j = tid; j < 4; j += 128) any |= blk[j] >= 0 ? a.count[h * a.nqb + blk[j]] : 0;
-    if (!__syncthreads_or(any)) {
+    if (tid < 4) s_qbs[tid] = 4 * t + tid < 2 * nqt ? pr[4 * t + tid] : -1;
+    __syncthreads();
+    if (!gather_lists(a, h, s_qbs, 4, qm, s_off)) {
       if (tid == 0) a.seg_count[w] = 0;
       return;
     }
-    for (int b = tid; b < a.list_blocks; b += 128) qm[b] = 0u;
-    __syncthreads();
     unsigned int maskA = 0u, maskB = 0u;
-    for (int j = 0; j < 4; ++j) {
-      if (blk[j] < 0) continue;
-      (j < 2 ? maskA : maskB) |= 1u << j;
-      const int n = a.count[h * a.nqb + blk[j]];
-      const int* lst = a.blocks + ((size_t)h * a.nqb + blk[j]) * a.cap;
-      for (int e = tid; e < n; e += 128) {
-        const int b = lst[e];
-        if (b >= 0 && b < a.list_blocks) atomicOr(&qm[b], 1u << j);
-      }
-    }
-    __syncthreads();
+    for (int j = 0; j < 4; ++j)
+      if (s_qbs[j] >= 0) (j < 2 ? maskA : maskB) |= 1u << j;
     emit_plan_segments<4>(qm, a.list_blocks, a.kt, maskA, maskB, true,
                           a.segs + (size_t)w * a.seg_cap, a.seg_cap, a.seg_count + w, cnt);
     return;
@@ -287,24 +313,13 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
     mid = q0 + kTileRows < q1 ? q0 + kTileRows : q1;
   }
   const int qb0 = a.qt.block_of(q0), qb1 = a.qt.block_of(q1 - 1);
-  int any = 0;
-  for (int j = tid; j <= qb1 - qb0 && j < 32; j += 128) any |= a.count[h * a.nqb + qb0 + j];
-  if (!__syncthreads_or(any)) {
+  const int nq = qb1 - qb0 + 1 < 32 ? qb1 - qb0 + 1 : 32;
+  if (tid < 32) s_qbs[tid] = tid < nq ? qb0 + tid : -1;
+  __syncthreads();
+  if (!gather_lists(a, h, s_qbs, nq, qm, s_off)) {
     if (tid == 0) a.seg_count[w] = 0;
     return;
   }
-  for (int b = tid; b < a.list_blocks; b += 128) qm[b] = 0u;
-  __syncthreads();
-  for (int j = 0; j <= qb1 - qb0 && j < 32; ++j) {
-    const int qb = qb0 + j;
-    const int n = a.count[h * a.nqb + qb];
-    const int* lst = a.blocks + ((size_t)h * a.nqb + qb) * a.cap;
-    for (int e = tid; e < n; e += 128) {
-      const int b = lst[e];
-      if (b >= 0 && b < a.list_blocks) atomicOr(&qm[b], 1u << j);
-    }
-  }
-  __syncthreads();
   auto bits = [&](int r0, int r1) -> unsigned int {
     if (r0 >= r1) return 0u;
     int lo = a.qt.block_of(r0) - qb0, hi = a.qt.block_of(r1 - 1) - qb0;

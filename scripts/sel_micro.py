@@ -44,7 +44,7 @@ def run(H, chunk, s_i, topk=6, f=3, bpf=25, d=128, exact=0, reps=200):
     return e0.elapsed_time(e1) / (reps // 20 * 20) * 1e3
 
 
-if len(sys.argv) > 1:  # one case, a few plain launches (for ncu): name H
+if len(sys.argv) > 1 and sys.argv[1] != "plan":  # one case, a few plain launches (for ncu): name H
     cfg = {"c2": (7, 6 / 7), "c5_s70": (7, 0.7), "c3": (14, 0.9046)}[sys.argv[1]]
     H = int(sys.argv[2])
     nqb, P = 75, (cfg[0] - 1) * 3
@@ -56,6 +56,55 @@ if len(sys.argv) > 1:  # one case, a few plain launches (for ncu): name H
     torch.cuda.synchronize()
     sys.exit(0)
 
-for chunk, s_i, name in [(7, 6 / 7, "c2"), (7, 0.7, "c5_s70"), (14, 0.9046, "c3")]:
+for chunk, s_i, name in [] if len(sys.argv) > 1 else [(7, 6 / 7, "c2"), (7, 0.7, "c5_s70"), (14, 0.9046, "c3")]:
     for H in (1, 4, 12):
         print(name, "H", H, "screened %.1f us" % run(H, chunk, s_i), "exact %.1f us" % run(H, chunk, s_i, exact=1))
+
+
+def graph_time(fn, reps=200):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(20):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps // 20):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (reps // 20 * 20) * 1e3
+
+
+def plan_pair(chunk, s_i, H=12, f=3, n=1560, d=128, topk=6):
+    """pairing and plan-kernel times on the selections of random summaries"""
+    qt = D.TilingSpec(f * n, n, 64)
+    kt = D.TilingSpec(chunk * f * n, n, 64)
+    bpf = -(-n // 64)
+    P = (chunk - 1) * f
+    qb = torch.randn((H, qt.count, d), device=dev) * 0.125
+    kb = torch.randn((H, kt.count, d), device=dev) * 0.125
+    kf = torch.randn((H, P, d), device=dev) * 0.05
+    sel = D.select(qb, kb, kf, bpf, chunk, f, topk, False, s_i)
+    lb = P * bpf
+    qperm = D.pair_qblocks(sel.blocks, sel.count, lb)
+    tp = graph_time(lambda: D.pair_qblocks(sel.blocks, sel.count, lb))
+    out = {"pair": tp}
+    for mode in (0, 1, 2):
+        with D.qtile_scope(mode):
+            out[f"plan{mode}"] = graph_time(
+                lambda: D.plan_tiles(sel.blocks, sel.count, qt, kt, lb,
+                                     qperm=qperm if mode == 2 else None))
+    return out
+
+
+if len(sys.argv) == 1 or sys.argv[1] == "plan":
+    for chunk, s_i, name in [(7, 0.5, "c5_s50"), (7, 0.7, "c5_s70"), (14, 0.9046, "c3")]:
+        print(name, {k: round(v, 1) for k, v in plan_pair(chunk, s_i).items()}, "us")
