@@ -526,6 +526,9 @@ def run_ours(args, c):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_chunk_r = float(t.item())
     clk = clocks.stop()
+    if os.environ.get("LF_BENCH_TIMELINE") and rank == 0:
+        timeline_dump(lambda: g_chunk.replay(), os.environ["LF_BENCH_TIMELINE"])
+        timeline_dump(chunk_flow, os.environ["LF_BENCH_TIMELINE"] + ".eager.csv")
     value = flops_r_step / (ms_chunk_r * 1e-3) / 1e12
     errs += int(ro.err.item())
 
@@ -852,6 +855,32 @@ def run_ours(args, c):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def timeline_dump(fn, path: str, reps: int = 3) -> None:
+    """LF_BENCH_TIMELINE=path: the device timeline of `reps` replays (kernel and
+    copy intervals per stream, CUPTI via torch.profiler) as CSV -- where the
+    rollout step's time goes beyond the attention kernel (profiling aid; not a
+    bench number)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+    rows = []
+    for ev in prof.events():
+        if ev.device_type.name != "CUDA":
+            continue
+        rows.append((ev.time_range.start, ev.time_range.end - ev.time_range.start,
+                     getattr(ev, "device_resource_id", -1), ev.name[:90]))
+    rows.sort()
+    t0 = rows[0][0] if rows else 0
+    with open(path, "w") as fh:
+        fh.write("start_us,dur_us,stream,name\n")
+        for st, du, sid, nm in rows:
+            fh.write(f"{st - t0:.2f},{du:.2f},{sid},\"{nm}\"\n")
 
 
 def self_launch(args) -> int:

@@ -147,6 +147,18 @@ int opt(int i) {
 }
 
 // SM count of the current device (cached per device ordinal)
+// The selection-side kernels (pool q, select, pair, plan) of step s+1 run on a
+// side stream while step s's persistent attention kernel holds every SM with
+// ~200 KB of shared memory.  An SM only takes CTAs of kernels whose preferred
+// L1 / shared-memory split it can keep, so these kernels ask for the same
+// (maximum-shared) carveout as the attention kernel and can be co-resident
+// instead of waiting for it to drain.  Host-side attribute, no stream work.
+template <class K>
+static void share_sm(K* kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
+}
+
 int sm_count() {
   static std::atomic<int> cache[64];
   int dev = 0;
@@ -203,6 +215,7 @@ int launch_pool_t(const PoolArgs& a, int vec, int ns, cudaStream_t st) {
   dim3 grid((unsigned)((warps * 32 + 255) / 256));
 #define LF_POOL(V, N)                                        \
   if (vec == V && ns == N) {                                 \
+    share_sm(pool_kernel<T, V, N>);                          \
     pool_kernel<T, V, N><<<grid, 256, 0, st>>>(a);           \
     return check_launch("pool_kernel");                      \
   }
@@ -691,6 +704,34 @@ int lf_pool_blocks(const lf_mat* x, lf_tiling tiling, int32_t max_blocks, float*
   if ((rc = check_mat(x, "x")) || (rc = check_tiling(tiling, "tiling"))) return rc;
   if (tiling.total != x->rows) return fail(LF_ERR_INVALID, "tiling total != rows");
   if (x->d > 256) return fail(LF_ERR_UNSUPPORTED, "d > 256");
+  {
+    // bf16 contiguous whole frames (query pooling of a rollout step): the TMA
+    // frame kernel, each frame split into block ranges so that the grid covers
+    // the SMs (12 heads x 3 frames alone would be 36 CTAs)
+    const int per = (tiling.period + tiling.block - 1) / tiling.block;
+    const int frames = tiling.period > 0 ? tiling.total / tiling.period : 0;
+    const int count = frames * per;
+    if (x->dtype == LF_BF16 && (x->d == 128 || x->d == 64) && x->row_stride == x->d &&
+        x->head_stride % 8 == 0 && reinterpret_cast<uintptr_t>(x->ptr) % 16 == 0 &&
+        tiling.block <= 64 && frames > 0 && tiling.total % tiling.period == 0 &&
+        (max_blocks < 0 || max_blocks >= count) && out_head_stride == (int64_t)count * x->d &&
+        reinterpret_cast<uintptr_t>(out) % 8 == 0 && opt(LF_OPT_POOL_NO_TMA) != 1) {
+      FramePoolArgs fa;
+      memset(&fa, 0, sizeof(fa));
+      fa.q = static_cast<const __nv_bfloat16*>(x->ptr);
+      fa.q_row = x->row_stride; fa.q_head = x->head_stride;
+      fa.heads = x->heads; fa.d = x->d; fa.period = tiling.period; fa.block = tiling.block;
+      fa.per_period = per;
+      fa.q_frames = frames;
+      const int want = 2 * sm_count();
+      int split = (want + x->heads * frames - 1) / (x->heads * frames);
+      split = split < 1 ? 1 : (split > per ? per : split);
+      fa.q_split = split;
+      fa.q_block = out;
+      launch_frame_pool_tma(fa, x->d, 0, x->heads * frames * split, stream);
+      return check_launch("pool_frames_tma_kernel");
+    }
+  }
   PoolArgs a;
   a.njobs = 1;
   a.job[0] = make_job(x, tiling, max_blocks, out, out_head_stride);
@@ -732,6 +773,7 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
       fa.q_frames = q_tiling.total / q_tiling.period;
       fa.k_frames = k_tiling.total / k_tiling.period;
       fa.past_frames = past_frames;
+      fa.q_split = 1;
       fa.q_block = q_block; fa.k_block = k_block; fa.k_frame = k_frame;
       fa.kb_head = (long long)fa.k_frames * per * d;
       fa.kf_head = (long long)past_frames * d;
@@ -814,6 +856,7 @@ int lf_pool_chunk_k(const lf_mat* k, lf_tiling k_tiling, int32_t blocks_per_fram
   fa.heads = k->heads; fa.d = d; fa.period = k_tiling.period; fa.block = k_tiling.block;
   fa.per_period = per;
   fa.q_frames = 0;
+  fa.q_split = 1;
   fa.k_frames = k_tiling.total / k_tiling.period;
   fa.past_frames = fa.k_frames;  // every frame of a committed chunk is a past frame
   fa.k_block = k_block; fa.k_frame = k_frame;
@@ -851,6 +894,7 @@ static int select_launch(const float* q_block, const float* k_block, int64_t kb_
   // one 4-warp CTA per (head, query block)
   if (lay.bytes > 48 * 1024)
     cudaFuncSetAttribute(select_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.bytes);
+  share_sm(select_screen_kernel);
   select_screen_kernel<<<heads * nqb, kSelThreads, lay.bytes, S(stream)>>>(a);
   return check_launch("select_screen_kernel");
 }
@@ -916,6 +960,7 @@ int lf_pair_qblocks(const int32_t* blocks, const int32_t* count, int32_t heads, 
     cudaFuncSetAttribute(pair_qblocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   PairArgs a{blocks, count, nqb, cap, lb, words, qperm};
+  share_sm(pair_qblocks_kernel);
   pair_qblocks_kernel<<<heads, kPairThreads, smem, S(stream)>>>(a);
   return check_launch("pair_qblocks_kernel");
 }
@@ -950,6 +995,7 @@ int lf_plan_tiles_paired(const int32_t* blocks, const int32_t* count, int32_t he
   if (qmode || opt(LF_OPT_PLAN_WARP) != 1) {  // the warp planner knows 128/256-row tiles only
     if (spw > 48 * 1024)
       cudaFuncSetAttribute(plan_tiles_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, spw);
+    share_sm(plan_tiles_cta_kernel);
     plan_tiles_cta_kernel<<<heads * ntiles, 128, spw, S(stream)>>>(a);
     return check_launch("plan_tiles_cta_kernel");
   }

@@ -168,6 +168,7 @@ struct FramePoolArgs {
   long long q_row, q_head, k_row, k_head;  // element strides
   int heads, d, period, block, per_period;
   int q_frames, k_frames, past_frames;
+  int q_split;     // CTAs per query frame (TMA kernel; each pools a contiguous block range)
   float* q_block;  // [H][q_frames*bpf][d]
   float* k_block;  // [H][k_frames*bpf][d]
   float* k_frame;  // [H][past_frames][d]
@@ -190,11 +191,14 @@ __global__ void __launch_bounds__(512) pool_frames_bf16_kernel(FramePoolArgs a) 
   constexpr int GROUPS = 512 / LPB;
   constexpr int UNROLL = 8;
   extern __shared__ float fp_smem[];  // [bpf][d] block means of this frame (key frames)
-  const int nfr = a.q_frames + a.k_frames;
+  const int nq = a.q_frames * a.q_split;  // query frames are split into q_split block ranges
+  const int nfr = nq + a.k_frames;
   const int h = blockIdx.x / nfr;
   const int fr = blockIdx.x - h * nfr;
-  const bool is_q = fr < a.q_frames;
-  const int frame = is_q ? fr : fr - a.q_frames;
+  const bool is_q = fr < nq;
+  const int frame = is_q ? fr / a.q_split : fr - nq;
+  const int part = is_q ? fr - frame * a.q_split : 0, nparts = is_q ? a.q_split : 1;
+  const int j0 = part * a.per_period / nparts, j1 = (part + 1) * a.per_period / nparts;
   const __nv_bfloat16* base =
       is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
   const long long rs = is_q ? a.q_row : a.k_row;
@@ -307,11 +311,14 @@ __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frame
   uint64_t* full = reinterpret_cast<uint64_t*>(pt_smem + C::NST * C::STAGE);
   uint64_t* empty = full + C::NST;
   float* fp_smem = reinterpret_cast<float*>(empty + C::NST);  // [per_period][D]
-  const int nfr = a.q_frames + a.k_frames;
+  const int nq = a.q_frames * a.q_split;  // query frames are split into q_split block ranges
+  const int nfr = nq + a.k_frames;
   const int h = blockIdx.x / nfr;
   const int fr = blockIdx.x - h * nfr;
-  const bool is_q = fr < a.q_frames;
-  const int frame = is_q ? fr : fr - a.q_frames;
+  const bool is_q = fr < nq;
+  const int frame = is_q ? fr / a.q_split : fr - nq;
+  const int part = is_q ? fr - frame * a.q_split : 0, nparts = is_q ? a.q_split : 1;
+  const int j0 = part * a.per_period / nparts, j1 = (part + 1) * a.per_period / nparts;
   const __nv_bfloat16* base = is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
   float* out = is_q ? a.q_block + ((long long)h * a.q_frames * a.per_period) * D
                     : a.k_block + (long long)h * a.kb_head;
@@ -328,13 +335,13 @@ __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frame
   const int fe = frame * a.period + a.period;
   if (warp == 0) {
     if (threadIdx.x == 0) {
-      for (int j = 0; j < a.per_period; ++j) {
+      for (int j = j0; j < j1; ++j) {
         const int r0 = frame * a.period + j * a.block;
         int r1 = r0 + a.block;
         r1 = r1 < fe ? r1 : fe;
-        const int st = j % C::NST;
+        const int st = (j - j0) % C::NST;
         const uint32_t bytes = (uint32_t)(r1 - r0) * D * 2;
-        mbar_wait(empty + st, ((j / C::NST) & 1) ^ 1);
+        mbar_wait(empty + st, (((j - j0) / C::NST) & 1) ^ 1);
         mbar_expect_tx(full + st, bytes);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -348,12 +355,13 @@ __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frame
   const int t = threadIdx.x - 32;
   const int grp = t / (D / 2);        // consumer group: blocks j with j % G == grp
   const int col = (t % (D / 2)) * 2;  // this thread's column pair
-  for (int j = grp; j < a.per_period; j += G) {
+  for (int jj = grp; jj < j1 - j0; jj += G) {
+    const int j = j0 + jj;
     const int r0 = frame * a.period + j * a.block;
     int r1 = r0 + a.block;
     r1 = r1 < fe ? r1 : fe;
-    const int st = j % C::NST;
-    mbar_wait(full + st, (j / C::NST) & 1);
+    const int st = jj % C::NST;
+    mbar_wait(full + st, (jj / C::NST) & 1);
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(ring + st * C::STAGE) + col / 2;
     const int n = r1 - r0;
     double a0 = 0.0, a1 = 0.0;

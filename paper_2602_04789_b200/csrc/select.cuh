@@ -599,6 +599,7 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
     a.out_budget[0] = total;
     a.out_budget[1] = past_budget;
     a.out_budget[2] = total < current;
+    a.out_budget[3] = 0;
   }
   __syncthreads();
   // screening bound scale gamma |q|_2, rounded upward

@@ -196,7 +196,7 @@ def select(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: int, p
     blocks = torch.empty((H, nqb, cap), dtype=torch.int32, device=dev)
     count = torch.empty((H, nqb), dtype=torch.int32, device=dev)
     frames = torch.empty((H, nqb, frame_cap), dtype=torch.int32, device=dev)
-    budget = torch.zeros(4, dtype=torch.int32, device=dev)
+    budget = torch.empty(4, dtype=torch.int32, device=dev)  # all four written by the kernel
     scores = torch.empty((H, nqb, cap), dtype=torch.float64, device=dev) if want_scores else None
     fscores = torch.empty((H, nqb, max(P, 1)), dtype=torch.float64, device=dev) if want_scores else None
     for t in (q_block, k_block, k_frame):
@@ -309,7 +309,7 @@ def select_plan(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: i
     blocks = torch.empty((H, nqb, cap), dtype=torch.int32, device=dev)
     count = torch.empty((H, nqb), dtype=torch.int32, device=dev)
     frames = torch.empty((H, nqb, frame_cap), dtype=torch.int32, device=dev)
-    budget = torch.zeros(4, dtype=torch.int32, device=dev)
+    budget = torch.empty(4, dtype=torch.int32, device=dev)  # all four written by the kernel
     margin = torch.empty((H, nqb, 2), dtype=torch.float64, device=dev) if want_margin else None
     rows = plan_rows()
     ntiles = int(lib.lf_plan_tile_count(qt.abi()))
