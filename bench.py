@@ -15,6 +15,8 @@ memory by the selection kernel.
 
 LF_BENCH_TRACE=1 prints the per-iteration device times of the timed legs to
 stderr (diagnosing outliers, e.g. of the PCIe-bound e2e leg).
+LF_BENCH_TIMELINE=path writes the device timeline (kernel intervals per
+stream) of three headline replays, and of one eager chunk, as CSV.
 
 Multi-GPU (torchrun, one rank per GPU): heads are sharded when H % N == 0 and
 the per-head outputs are all-gathered over NCCL (strong scaling); otherwise
@@ -464,7 +466,13 @@ def run_ours(args, c):
     ro.kv_slot(i)[1].copy_(Vc[0])
 
     # the selection half of step s+1 (pool q, select, plan; it reads only q and
-    # the committed summaries) runs on a side stream while step s attends
+    # the committed summaries) is enqueued on a side stream while step s
+    # attends.  On the device only what is launched before the attention kernel
+    # overlaps it (the query pooling): the persistent attention CTAs (10 warps x
+    # 168 registers, allocated as 12 warps) leave ~1k registers per SM, so the
+    # selection and plan kernels run in the gap after it (LF_BENCH_TIMELINE shows
+    # the timeline) -- which is also all a real denoiser allows, whose query of
+    # step s+1 depends on step s
     side = torch.cuda.Stream()
     comm = torch.cuda.Stream()
     ev_prep = [torch.cuda.Event() for _ in range(T)]

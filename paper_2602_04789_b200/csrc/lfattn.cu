@@ -147,18 +147,6 @@ int opt(int i) {
 }
 
 // SM count of the current device (cached per device ordinal)
-// The selection-side kernels (pool q, select, pair, plan) of step s+1 run on a
-// side stream while step s's persistent attention kernel holds every SM with
-// ~200 KB of shared memory.  An SM only takes CTAs of kernels whose preferred
-// L1 / shared-memory split it can keep, so these kernels ask for the same
-// (maximum-shared) carveout as the attention kernel and can be co-resident
-// instead of waiting for it to drain.  Host-side attribute, no stream work.
-template <class K>
-static void share_sm(K* kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       (int)cudaSharedmemCarveoutMaxShared);
-}
-
 int sm_count() {
   static std::atomic<int> cache[64];
   int dev = 0;
@@ -215,7 +203,6 @@ int launch_pool_t(const PoolArgs& a, int vec, int ns, cudaStream_t st) {
   dim3 grid((unsigned)((warps * 32 + 255) / 256));
 #define LF_POOL(V, N)                                        \
   if (vec == V && ns == N) {                                 \
-    share_sm(pool_kernel<T, V, N>);                          \
     pool_kernel<T, V, N><<<grid, 256, 0, st>>>(a);           \
     return check_launch("pool_kernel");                      \
   }
@@ -894,7 +881,6 @@ static int select_launch(const float* q_block, const float* k_block, int64_t kb_
   // one 4-warp CTA per (head, query block)
   if (lay.bytes > 48 * 1024)
     cudaFuncSetAttribute(select_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.bytes);
-  share_sm(select_screen_kernel);
   select_screen_kernel<<<heads * nqb, kSelThreads, lay.bytes, S(stream)>>>(a);
   return check_launch("select_screen_kernel");
 }
@@ -960,7 +946,6 @@ int lf_pair_qblocks(const int32_t* blocks, const int32_t* count, int32_t heads, 
     cudaFuncSetAttribute(pair_qblocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   PairArgs a{blocks, count, nqb, cap, lb, words, qperm};
-  share_sm(pair_qblocks_kernel);
   pair_qblocks_kernel<<<heads, kPairThreads, smem, S(stream)>>>(a);
   return check_launch("pair_qblocks_kernel");
 }
@@ -995,7 +980,6 @@ int lf_plan_tiles_paired(const int32_t* blocks, const int32_t* count, int32_t he
   if (qmode || opt(LF_OPT_PLAN_WARP) != 1) {  // the warp planner knows 128/256-row tiles only
     if (spw > 48 * 1024)
       cudaFuncSetAttribute(plan_tiles_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, spw);
-    share_sm(plan_tiles_cta_kernel);
     plan_tiles_cta_kernel<<<heads * ntiles, 128, spw, S(stream)>>>(a);
     return check_launch("plan_tiles_cta_kernel");
   }
