@@ -334,6 +334,44 @@ __device__ __forceinline__ int screen_decide(const float* s, const float* b, int
                                              int* m_out) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int nseg = n > 0 ? (n + seglen - 1) / seglen : 0;
+  if (nseg == 1 && n <= 32) {
+    // one top-k of at most 32 items (the frame list): a single warp decides it
+    // with shuffles and warp reductions, the CTA waits at one barrier
+    __shared__ int s_st, s_m;
+    if (tid < 32) {
+      constexpr unsigned FULL = 0xffffffffu;
+      const bool h = lane < n;
+      const float v = h ? s[lane] : 0.f, bv = h ? b[lane] : 0.f;
+      const int k = cut(0);
+      const bool decide = k > 0 && k < n;
+      int r = 0;
+      for (int j = 0; j < n; ++j) r += __shfl_sync(FULL, v, j) > v;
+      const bool in = h && (decide ? r < k : k > 0);
+      if (h) flag[lane] = in;
+      const bool bad = __any_sync(FULL, h && !(isfinite(v) && isfinite(bv)));
+      int st = bad ? 2 : 0, m = 0;
+      if (!bad && decide) {
+        const int lo = in ? ford(__fsub_rd(v, bv)) : 0x7fffffff;
+        const int hi = h && !in ? ford(__fadd_ru(v, bv)) : (int)0x80000000;
+        const int tin = __reduce_min_sync(FULL, lo), tout = __reduce_max_sync(FULL, hi);
+        if (__popc(__ballot_sync(FULL, in)) != k) {
+          st = 2;
+        } else if (!(tin > tout)) {
+          const bool amb = h && (in ? lo <= tout : hi >= tin);
+          if (amb) flag[lane] = 2;
+          m = __popc(__ballot_sync(FULL, amb && in));
+          st = 1;
+        }
+      }
+      if (lane == 0) {
+        s_st = st;
+        s_m = m;
+      }
+    }
+    __syncthreads();
+    *m_out = s_m;
+    return s_st;
+  }
   for (int j = tid; j < nseg; j += kSelThreads) {
     seg[3 * j] = 0x7fffffff;            // lowest selected lower end
     seg[3 * j + 1] = (int)0x80000000;  // highest rejected upper end
@@ -579,6 +617,7 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
   __shared__ double mred[8];
 
   __shared__ float s_qn[4];
+  const float* kf = a.k_frame + (size_t)h * a.kf_head_stride;
   const float* qrow = a.q_block + ((size_t)h * a.nqb + r) * d;
   float qn = 0.f;  // |q|^2, rounded upward
 #pragma unroll 1
@@ -609,7 +648,6 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
 
   SEL_MARK(1);
   // frame scores and the top-k frames
-  const float* kf = a.k_frame + (size_t)h * a.kf_head_stride;
   const int kf_n = a.topk < P ? a.topk : P;
   const bool fvec = (d & 31) == 0 && (reinterpret_cast<uintptr_t>(kf) & 15) == 0;
   const bool fexact = a.exact || a.out_fscores || a.out_margin;
