@@ -166,10 +166,18 @@ def test_screened_selection_vs_oracle(D, case, exact, lfopt):
     qb, kb, kf = _summaries(zlib.crc32(repr(case).encode()) & 0xffff, H, qt.count, kt.count, P, d, ties)
     dev = torch.device("cuda")
     tq, tk, tf = (torch.from_numpy(a).to(dev) for a in (qb, kb, kf))
+    D.select_fallbacks(reset=True)
     with D.qtile_scope(qmode):
         sel, tiles, _ = D.select_plan(tq, tk, tf, bpf, chunk, f, topk, mode == "per-frame", s_i,
                                       qt, kt, P * bpf)
     torch.cuda.synchronize()
+    fb = D.select_fallbacks(reset=True)
+    if ties == "near" and not exact:
+        # rows one ulp apart straddle some cut: the screen must have handed lists
+        # to the exact path (whole or ambiguous items only)
+        assert fb[0] + fb[1] > 0, fb
+    if exact:
+        assert fb == (0, 0, 0, 0), fb  # no screening at all
     cnt = sel.count.cpu().numpy()
     blocks = sel.blocks.cpu().numpy()
     frames = sel.frames.cpu().numpy()
