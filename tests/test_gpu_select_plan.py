@@ -193,6 +193,50 @@ def test_screened_selection_vs_oracle(D, case, exact, lfopt):
             assert blocks[h, r, :cnt[h, r]].tolist() == [int(x) for x in ids], (h, r)
 
 
+@pytest.mark.parametrize("kind", ["huge", "tiny", "mixed"])
+@pytest.mark.parametrize("exact", [0, 1])
+def test_screened_selection_extreme_magnitudes(D, kind, exact, lfopt):
+    """Magnitudes where fp32 screening cannot work -- squares overflowing to
+    inf (huge), products underflowing to zero (tiny), rows 40 orders of
+    magnitude apart (mixed): the bounds or the finiteness check hand the
+    lists to the exact path, and the selections equal the oracle's."""
+    lfopt("select_exact", exact)
+    H, f, n, d, chunk, s_i, topk = 2, 3, 1560, 128, 7, 0.7, 6
+    bpf = -(-n // 64)
+    qt = D.TilingSpec(f * n, n, 64)
+    kt = D.TilingSpec(chunk * f * n, n, 64)
+    P = (chunk - 1) * f
+    qb, kb, kf = _summaries(zlib.crc32(kind.encode()) & 0xffff, H, qt.count, kt.count, P, d, False)
+    if kind == "huge":
+        kb *= np.float32(1e19)
+        kf *= np.float32(1e19)
+    elif kind == "tiny":
+        kb *= np.float32(1e-25)
+        kf *= np.float32(1e-25)
+        qb *= np.float32(1e-25)
+    else:
+        rng = np.random.default_rng(7)
+        kb *= (10.0 ** rng.integers(-20, 20, size=(H, kt.count, 1))).astype(np.float32)
+        kf *= (10.0 ** rng.integers(-20, 20, size=(H, max(P, 1), 1))).astype(np.float32)
+    dev = torch.device("cuda")
+    tq, tk, tf = (torch.from_numpy(a).to(dev) for a in (qb, kb, kf))
+    sel, _, _ = D.select_plan(tq, tk, tf, bpf, chunk, f, topk, False, s_i, qt, kt, P * bpf)
+    torch.cuda.synchronize()
+    cnt = sel.count.cpu().numpy()
+    blocks = sel.blocks.cpu().numpy()
+    frames = sel.frames.cpu().numpy()
+    past_budget = int(sel.budget.cpu().numpy()[1])
+    for h in range(H):
+        views = O.Views(qb[h], kb[h], kf[h][:P], bpf)
+        for r in range(qt.count):
+            p = O.frame_scores(views, r)
+            fr = O.select_frames(p, topk, chunk, f)
+            past = [int(t) for t in fr if t < P]
+            assert [int(t) for t in frames[h, r] if t >= 0] == past, (h, r)
+            _, ids, _ = O.select_blocks(views, r, fr, past_budget, "global")
+            assert blocks[h, r, :cnt[h, r]].tolist() == [int(x) for x in ids], (h, r)
+
+
 def _fp64_bound(views, r, rows):
     """Worst |x - x'| between two fp64 summation orders of <row, q_r>:
     2 * d * 2^-53 * sum|k q| (Higham's gamma_d, twice)."""
