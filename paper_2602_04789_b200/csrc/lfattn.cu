@@ -293,7 +293,7 @@ int max_qblocks_per_tile(lf_tiling qt, int rows = kTileRows) {
 // attention kernel must agree: both read it here.
 thread_local int g_qmode_scope = -1;  // automatic choice of the lf_hsa_* call in progress
 constexpr int kBlockTilesMinPast = 16;
-constexpr int kPairedMinPast = 100;
+constexpr int kPairedMinPast = 80;
 int qmode_for(lf_tiling qt) {
   int req = opt(LF_OPT_QTILE);  // lf_set_qtile_mode
   if (req < 0) req = g_env_qtile;
@@ -315,11 +315,11 @@ int auto_qmode(double s, int chunk, int f, int n, int b_kv, int topk) {
   past = past < cap ? past : cap;
   // every past block selected: all query blocks share one list, nothing to gain
   if (past < kBlockTilesMinPast || past >= (long long)P * bpf) return 0;
-  // whole retrieved frames (>= 100 past blocks per query block): blocks that
-  // retrieved the same frames select the same keys, so pairing them by
-  // overlap pays for its extra launch (~30 us at 12 heads): attention -17 %
-  // at c5_s50; below it the pairing costs more than it saves (c3 -7 %,
-  // c5_s70 +-0 on the rollout step; profiles/r02/qtile_paired_ab.txt)
+  // most of the retrieved frames (>= 80 past blocks per query block): blocks
+  // that retrieved the same frames select the same keys, so pairing them by
+  // overlap pays for its extra launch (~28 us at 12 heads): attention -17 %
+  // at c5_s50, -6 % at c5_s70 (rollout +2 %); below it the pairing costs more
+  // than it saves (c3, 25 past blocks: -6 %; profiles/r02/qtile_paired_ab.txt)
   return past >= kPairedMinPast ? 2 : 1;
 }
 struct QmodeScope {

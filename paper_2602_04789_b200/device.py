@@ -41,14 +41,14 @@ def set_qtile_mode(mode: int) -> None:
 
 
 BLOCK_TILES_MIN_PAST = 16  # csrc/lfattn.cu kBlockTilesMinPast
-PAIRED_MIN_PAST = 100      # csrc/lfattn.cu kPairedMinPast
+PAIRED_MIN_PAST = 80       # csrc/lfattn.cu kPairedMinPast
 
 
 def auto_qtile_mode(s_host, chunk: int, f: int, bpf: int, topk_frames: int) -> int:
     """Geometry for one step from the host s_i (mirrors auto_qmode in lfattn.cu):
     block-aligned tiles when the estimated past blocks per query block is >= 16
     and below all past blocks (a fully selected past gives every block one list),
-    paired by selection overlap from 100 past blocks on."""
+    paired by selection overlap from 80 past blocks on."""
     P = (chunk - 1) * f
     if P <= 0 or s_host is None or not (0.0 <= float(s_host) < 1.0):
         return 0

@@ -9,10 +9,10 @@ def test_auto_choice_at_the_bench_configs():
     # c2 / c5_s85: (almost) no past blocks -> 128-row tiles
     assert D.auto_qtile_mode(6 / 7, 7, 3, bpf, 6) == 0
     assert D.auto_qtile_mode(0.85, 7, 3, bpf, 6) == 0
-    # c3 (chunk 14, 25 past blocks per query block), c5_s70 (83) -> block-aligned
+    # c3 (chunk 14, 25 past blocks per query block) -> block-aligned
     assert D.auto_qtile_mode(0.904632706980882, 14, 3, bpf, 6) == 1
-    assert D.auto_qtile_mode(0.7, 7, 3, bpf, 6) == 1
-    # c5_s50: whole retrieved frames (150 past blocks) -> paired by selection overlap
+    # c5_s70 (83 past blocks), c5_s50 (whole retrieved frames, 150) -> paired by overlap
+    assert D.auto_qtile_mode(0.7, 7, 3, bpf, 6) == 2
     assert D.auto_qtile_mode(0.5, 7, 3, bpf, 6) == 2
     # c5_dense: every past block selected (topk covers all 18 frames) -> 128-row tiles
     assert D.auto_qtile_mode(0.0, 7, 3, bpf, 18) == 0
