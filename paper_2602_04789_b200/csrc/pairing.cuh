@@ -98,55 +98,40 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
   tr[1] = clock64();
 #endif
   if (total > 0) {
-    // pairwise overlaps (upper triangle, mirrored): a warp per block x, a lane
-    // per partner y (rows of odd word stride: conflict-free), over x's non-zero
-    // words only (a selection spans a few frames: ~6 of ~47 words at chunk 14)
-    for (int x = warp; x < n; x += NW) {
-      unsigned int nzm[2] = {0u, 0u};  // which of x's first 64 words are non-zero
-      for (int w = lane; w < W && w < 64; w += 32)
-        if (bits[x * W + w]) nzm[w >> 5] |= 1u << (w & 31);
-      nzm[0] = __reduce_or_sync(0xffffffffu, nzm[0]);
-      nzm[1] = __reduce_or_sync(0xffffffffu, nzm[1]);
-      for (int y = x + 1 + lane; y < n + lane; y += 32) {
-        if (y >= n) break;
-        int c = 0;
-        for (int hw = 0; hw < 2; ++hw) {
-          unsigned int m = nzm[hw];
-          while (m) {
-            const int w = 32 * hw + __ffs(m) - 1;
-            m &= m - 1;
-            c += __popc(bits[x * W + w] & bits[y * W + w]);
-          }
-        }
-        for (int w = 64; w < W; ++w) c += __popc(bits[x * W + w] & bits[y * W + w]);
-        c = c < 2047 ? c : 2047;  // keeps the packed proposal key positive
-        ov[x * n + y] = ov[y * n + x] = (unsigned short)c;
-      }
+    // pairwise overlaps (upper triangle, mirrored): one thread per pair (x < y),
+    // consecutive threads on consecutive y (rows of odd word stride: conflict-free
+    // reads of row y, broadcast of row x) -- every pair in flight at once instead
+    // of a warp walking its rows
+    for (int pi = tid; pi < n * n; pi += NT) {
+      const int x = pi / n, y = pi - x * n;
+      if (y <= x) continue;
+      const unsigned int* bx = bits + x * W;
+      const unsigned int* by = bits + y * W;
+      int c = 0;
+      for (int w = 0; w < W; ++w) c += __popc(bx[w] & by[w]);
+      c = c < 2047 ? c : 2047;  // keeps the packed proposal key positive
+      ov[x * n + y] = ov[y * n + x] = (unsigned short)c;
     }
     __syncthreads();
 #ifdef LF_PAIR_TRACE
     tr[2] = clock64();
 #endif
-    // mutual-best rounds; a warp per proposing block, key = (overlap, nearer, lower index)
+    // mutual-best rounds; a thread per proposing block scans its row of the
+    // overlap matrix, key = (overlap, nearer, lower index)
     for (int round = 0; round < n; ++round) {
-      for (int x = warp; x < n; x += NW) {
+      for (int x = tid; x < n; x += NT) {
         int best = -1;
         if (mate[x] < 0) {
           int key = -1;
-          for (int y = lane; y < n; y += 32) {
-            if (y == x || mate[y] >= 0) continue;
+          const unsigned short* row = ov + x * n;
+          for (int y = 0; y < n; ++y) {
             const int dist = y > x ? y - x : x - y;
-            const int kk = ((int)ov[x * n + y] << 20) | ((1023 - dist) << 10) | (1023 - y);
-            key = kk > key ? kk : key;
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const int other = __shfl_xor_sync(0xffffffffu, key, o);
-            key = other > key ? other : key;
+            const int kk = ((int)row[y] << 20) | ((1023 - dist) << 10) | (1023 - y);
+            key = (y != x && mate[y] < 0 && kk > key) ? kk : key;
           }
           best = key >= 0 ? 1023 - (key & 1023) : -1;
         }
-        if (lane == 0) prop[x] = best;
+        prop[x] = best;
       }
       if (tid == 0) s_new = 0;
       __syncthreads();
