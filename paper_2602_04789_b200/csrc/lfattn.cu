@@ -710,6 +710,7 @@ int lf_pool_blocks(const lf_mat* x, lf_tiling tiling, int32_t max_blocks, float*
       fa.heads = x->heads; fa.d = x->d; fa.period = tiling.period; fa.block = tiling.block;
       fa.per_period = per;
       fa.q_frames = frames;
+      fa.k_split = 1;
       const int want = 2 * sm_count();
       int split = (want + x->heads * frames - 1) / (x->heads * frames);
       split = split < 1 ? 1 : (split > per ? per : split);
@@ -761,6 +762,7 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
       fa.k_frames = k_tiling.total / k_tiling.period;
       fa.past_frames = past_frames;
       fa.q_split = 1;
+      fa.k_split = 1;
       fa.q_block = q_block; fa.k_block = k_block; fa.k_frame = k_frame;
       fa.kb_head = (long long)fa.k_frames * per * d;
       fa.kf_head = (long long)past_frames * d;
@@ -849,8 +851,21 @@ int lf_pool_chunk_k(const lf_mat* k, lf_tiling k_tiling, int32_t blocks_per_fram
   fa.k_block = k_block; fa.k_frame = k_frame;
   fa.kb_head = kb_head_stride;
   fa.kf_head = kf_head_stride;
-  launch_frame_pool_tma(fa, d, per * d * 4, k->heads * fa.k_frames, stream);
-  return check_launch("pool_frames_tma_kernel");
+  // a chunk is only H*f frames (36 CTAs at 12 heads): split the frames into block
+  // ranges so that the grid covers the SMs, then pool the frame summaries from
+  // the written block means in a second, tiny launch
+  const int want = 2 * sm_count();
+  int split = (want + k->heads * fa.k_frames - 1) / (k->heads * fa.k_frames);
+  split = split < 1 ? 1 : (split > per ? per : split);
+  fa.k_split = split;
+  launch_frame_pool_tma(fa, d, split == 1 ? per * d * 4 : 0, k->heads * fa.k_frames * split,
+                        stream);
+  if ((rc = check_launch("pool_frames_tma_kernel"))) return rc;
+  if (split > 1) {
+    frame_summary_kernel<<<k->heads * fa.past_frames, 128, 0, S(stream)>>>(fa);
+    return check_launch("frame_summary_kernel");
+  }
+  return LF_OK;
 }
 
 static int select_launch(const float* q_block, const float* k_block, int64_t kb_head_stride,

@@ -169,6 +169,7 @@ struct FramePoolArgs {
   int heads, d, period, block, per_period;
   int q_frames, k_frames, past_frames;
   int q_split;     // CTAs per query frame (TMA kernel; each pools a contiguous block range)
+  int k_split;     // CTAs per key frame (TMA kernel; > 1: k_frame by frame_summary_kernel)
   float* q_block;  // [H][q_frames*bpf][d]
   float* k_block;  // [H][k_frames*bpf][d]
   float* k_frame;  // [H][past_frames][d]
@@ -191,14 +192,11 @@ __global__ void __launch_bounds__(512) pool_frames_bf16_kernel(FramePoolArgs a) 
   constexpr int GROUPS = 512 / LPB;
   constexpr int UNROLL = 8;
   extern __shared__ float fp_smem[];  // [bpf][d] block means of this frame (key frames)
-  const int nq = a.q_frames * a.q_split;  // query frames are split into q_split block ranges
-  const int nfr = nq + a.k_frames;
+  const int nfr = a.q_frames + a.k_frames;  // one CTA per frame (q_split / k_split == 1)
   const int h = blockIdx.x / nfr;
   const int fr = blockIdx.x - h * nfr;
-  const bool is_q = fr < nq;
-  const int frame = is_q ? fr / a.q_split : fr - nq;
-  const int part = is_q ? fr - frame * a.q_split : 0, nparts = is_q ? a.q_split : 1;
-  const int j0 = part * a.per_period / nparts, j1 = (part + 1) * a.per_period / nparts;
+  const bool is_q = fr < a.q_frames;
+  const int frame = is_q ? fr : fr - a.q_frames;
   const __nv_bfloat16* base =
       is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
   const long long rs = is_q ? a.q_row : a.k_row;
@@ -311,18 +309,22 @@ __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frame
   uint64_t* full = reinterpret_cast<uint64_t*>(pt_smem + C::NST * C::STAGE);
   uint64_t* empty = full + C::NST;
   float* fp_smem = reinterpret_cast<float*>(empty + C::NST);  // [per_period][D]
-  const int nq = a.q_frames * a.q_split;  // query frames are split into q_split block ranges
-  const int nfr = nq + a.k_frames;
+  // frames are split into q_split / k_split contiguous block ranges, one CTA each
+  const int nq = a.q_frames * a.q_split, nk = a.k_frames * a.k_split;
+  const int nfr = nq + nk;
   const int h = blockIdx.x / nfr;
   const int fr = blockIdx.x - h * nfr;
   const bool is_q = fr < nq;
-  const int frame = is_q ? fr / a.q_split : fr - nq;
-  const int part = is_q ? fr - frame * a.q_split : 0, nparts = is_q ? a.q_split : 1;
+  const int frame = is_q ? fr / a.q_split : (fr - nq) / a.k_split;
+  const int nparts = is_q ? a.q_split : a.k_split;
+  const int part = is_q ? fr - frame * a.q_split : fr - nq - frame * a.k_split;
   const int j0 = part * a.per_period / nparts, j1 = (part + 1) * a.per_period / nparts;
   const __nv_bfloat16* base = is_q ? a.q + (long long)h * a.q_head : a.k + (long long)h * a.k_head;
   float* out = is_q ? a.q_block + ((long long)h * a.q_frames * a.per_period) * D
                     : a.k_block + (long long)h * a.kb_head;
-  const bool keep = !is_q && frame < a.past_frames;
+  // the frame summary needs all of the frame's block means: split key frames
+  // leave it to frame_summary_kernel
+  const bool keep = !is_q && frame < a.past_frames && nparts == 1;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NST; ++s) {
@@ -391,6 +393,21 @@ __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frame
     double s = (double)fp_smem[cc];
     for (int j = 1; j < a.per_period; ++j) s += (double)fp_smem[j * D + cc];
     kf[cc] = (float)(s / (double)a.per_period);
+  }
+}
+
+// k_frame of key frames pooled by split CTAs: the mean of the frame's block
+// means in block order, read back from k_block -- the same fp32 values, the
+// same fp64 block-order sum and division as the in-CTA path
+// (selection.py:109-113).  One CTA per (head, past frame).
+__global__ void __launch_bounds__(128) frame_summary_kernel(FramePoolArgs a) {
+  const int h = blockIdx.x / a.past_frames, frame = blockIdx.x - h * a.past_frames;
+  const float* kb = a.k_block + (long long)h * a.kb_head + (long long)frame * a.per_period * a.d;
+  float* kf = a.k_frame + (long long)h * a.kf_head + (long long)frame * a.d;
+  for (int c = threadIdx.x; c < a.d; c += blockDim.x) {
+    double s = (double)__ldg(kb + c);
+    for (int j = 1; j < a.per_period; ++j) s += (double)__ldg(kb + (long long)j * a.d + c);
+    kf[c] = (float)(s / (double)a.per_period);
   }
 }
 
