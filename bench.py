@@ -549,7 +549,6 @@ def run_ours(args, c):
     hint = D.past_tiles_hint(s_host, i, f, bpf, c["topk"], qt)
     qmode = D.auto_qtile_mode(s_host, i, f, bpf, c["topk"])  # as HsaRollout.prepare picks it
     from paper_2602_04789_b200 import _lib as LL
-    kernel_used = int(LL.lib().lf_attention_kernel_choice(h_local, lq, lq, hint))
     stage = {"pool": [], "select": [], "attn": []}
     graphs = []
     for s in range(T):
@@ -826,8 +825,7 @@ def run_ours(args, c):
                           "e2e_value": flops_step / (e2e_ms_sl * 1e-3) / 1e12,
                           "e2e_ms_per_chunk": e2e_ms_sl, "e2e_h2d_bytes_per_step": h2d_sl},
             "roofline": {"bound": "tensor",
-                         "kernel": ("attn_fwd_v5_kernel<128> (query-tile pairs)" if kernel_used == 5
-                                    else "attn_fwd_v7_kernel<128> (query tile, two softmax sets)"),
+                         "kernel": "attn_fwd_v7_kernel<128> (query tile, two softmax sets)",
                          "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
                          "frac": achieved_tf / tf_peak,
                          "traffic": (traffic.get("attn_fwd", {}).get("bytes")

@@ -217,19 +217,16 @@ int lf_attention(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_tiling q_
                  int64_t out_row_stride, int64_t out_head_stride, float* lse, int32_t* err_flag,
                  void* stream);
 
-/* lf_attention with an explicit kernel choice (same results within the stated
- * tolerance, bit-exact masks either way):
- *   LF_KERNEL_AUTO  the library's choice (currently the tile kernel, which
- *                   matched or beat the pair kernel at every measured shape);
- *                   past_tiles_hint (estimated non-dense key tiles per
- *                   256-row plan tile, -1 = unknown) is reserved for it
+/* lf_attention with an explicit kernel choice:
+ *   LF_KERNEL_AUTO  the library's choice (the tile kernel); past_tiles_hint
+ *                   (estimated non-dense key tiles per 256-row plan tile,
+ *                   -1 = unknown) is reserved for it
  *   LF_KERNEL_TILE  one 128-row query tile per CTA, two softmax sets on
  *                   alternating key tiles (attn_fwd_v7_kernel)
- *   LF_KERNEL_PAIR  two query tiles per CTA in ping-pong sharing K/V, stream-K
- *                   tail (attn_fwd_v5_kernel) */
+ * Any other value is LF_ERR_INVALID (round 1's query-tile-pair kernel, 5, was
+ * removed: the tile kernel matched or beat it everywhere). */
 #define LF_KERNEL_AUTO 0
 #define LF_KERNEL_TILE 3
-#define LF_KERNEL_PAIR 5
 /* The kernel LF_KERNEL_AUTO picks for this problem (reporting). */
 int lf_attention_kernel_choice(int32_t heads, int32_t q_rows, int32_t dense_keys,
                                int32_t past_tiles_hint);
@@ -309,7 +306,7 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
                                  list (no fp32 screening)                          */
 #define LF_OPT_ATTN_DEBUG 6   /* LF_ATTN_DEBUG: 1 skip softmax, 2 event trace        */
 #define LF_OPT_ATTN_POLY 7    /* LF_ATTN_POLY: polynomial exp2 on every n-th pair    */
-#define LF_OPT_ATTN_KERNEL 8  /* LF_ATTN_VER (5/7): forced attention kernel, 0 auto  */
+#define LF_OPT_ATTN_KERNEL 8  /* LF_ATTN_VER (7): forced attention kernel, 0 auto      */
 #define LF_OPT_QTILE 9        /* LF_QTILE (blocks|paired|rows) / lf_set_qtile_mode    */
 #define LF_OPT_TRACE_CTA 10   /* LF_ATTN_TRACE_CTA                                   */
 #define LF_OPT_COUNT 11

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "liblfattn.so")
 LF_OK, LF_ERR_INVALID, LF_ERR_CUDA, LF_ERR_UNSUPPORTED = 0, 1, 2, 3
 LF_ERR_ZERO_ACTIVE_ROW, LF_ERR_DEGENERATE, LF_ERR_NO_DRIVER = 4, 5, 6
 LF_F32, LF_BF16 = 0, 1
-LF_KERNEL_AUTO, LF_KERNEL_TILE, LF_KERNEL_PAIR = 0, 3, 5
+LF_KERNEL_AUTO, LF_KERNEL_TILE = 0, 3
 
 # every symbol include/lfattn.h declares (checked by tests/test_abi.py)
 EXPORTS = (

@@ -34,13 +34,10 @@ struct AttnParams {
   int* err;
   // load balancing.  Tile kernel: items [0, full_items) run whole, each of the
   // remaining "tail" items is cut into tail_split parts over its key tiles.
-  // Pair kernel: whole items [0, full_items) round-robin, the tail stream-K.
   // Parts write unnormalised partials; the last one to finish merges them.
   int full_items, tail_split;
   int debug;  // benchmarking probe: 1 = skip softmax arithmetic (P left as S bits), 2 = trace
   long long* trace;  // debug == 2: clock64 event trace of CTA 0 (v5)
-  CUtensorMap to;    // v5: bf16 output map (box 64 cols x 32 rows), valid when tma_out
-  int tma_out;
   int plan_pairs;    // segs are 256-row (pair) plans
   int qmode;         // query-tile geometry (qtile_rows in common.cuh); 1, 2 imply plan_pairs
   const int* qperm;  // geometry 2: [H][2 * n_qtiles] query block of each 64-row tile half
@@ -221,6 +218,56 @@ __device__ __forceinline__ void store_row(const AttnParams& p, int h, int grow, 
           pack_bf16(v[e] * inv, v[e + 1] * inv), pack_bf16(v[e + 2] * inv, v[e + 3] * inv),
           pack_bf16(v[e + 4] * inv, v[e + 5] * inv), pack_bf16(v[e + 6] * inv, v[e + 7] * inv));
   }
+}
+
+// tcgen05 / warp helpers of the attention kernel
+// 32 lanes x 8 columns of 32-bit: thread i writes lane (base+i)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+// tcgen05.mma / commit issued by one elected lane of a converged warp
+__device__ __forceinline__ void tc_mma_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ long long clk64() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
 }
 
 }  // namespace lf

@@ -19,7 +19,7 @@
 // P_X overwrites the first 64 columns of S_X.  Q stays in shared memory (SS QK).
 // Issue order:  QK_0(t0) QK_1(t1) PV_0(t0) QK_0(t2) PV_1(t1) QK_1(t3) ...
 #pragma once
-#include "attn_sm100_v5.cuh"
+#include "attn_common.cuh"
 
 namespace lf {
 

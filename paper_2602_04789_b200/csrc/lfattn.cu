@@ -9,7 +9,6 @@
 #include <algorithm>
 #include <atomic>
 
-#include "attn_sm100_v5.cuh"
 #include "attn_sm100_v7.cuh"
 #include "cag.cuh"
 #include "pairing.cuh"
@@ -64,19 +63,6 @@ EncodeTiledFn encoder() {
 }
 
 // 3-D map (d, rows, heads) over a bf16 lf_mat, 64-column x box_rows boxes, 128B swizzle
-// bf16 output [H][Lq][d] (row / head strides in elements) for the v5 TMA-store epilogue
-bool make_out_map(CUtensorMap* map, void* out, int d, int Lq, int H, long long rs, long long hs) {
-  EncodeTiledFn enc = encoder();
-  if (!enc || reinterpret_cast<uintptr_t>(out) % 16 || (rs * 2) % 16 || (hs * 2) % 16) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)Lq, (cuuint64_t)H};
-  cuuint64_t strides[2] = {(cuuint64_t)rs * 2, (cuuint64_t)hs * 2};
-  cuuint32_t box[3] = {64, 32, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, out, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 int make_map(CUtensorMap* map, const lf_mat* m, int box_rows) {
   EncodeTiledFn enc = encoder();
   if (!enc) return fail(LF_ERR_NO_DRIVER, "cuTensorMapEncodeTiled unavailable");
@@ -133,7 +119,7 @@ void init_options() {
     g_opt[LF_OPT_ATTN_DEBUG].store(env_int("LF_ATTN_DEBUG", 0));
     g_opt[LF_OPT_ATTN_POLY].store(env_int("LF_ATTN_POLY", 0));
     const int ver = env_int("LF_ATTN_VER", 0);
-    g_opt[LF_OPT_ATTN_KERNEL].store(ver == 5 ? LF_KERNEL_PAIR : ver == 7 ? LF_KERNEL_TILE : 0);
+    g_opt[LF_OPT_ATTN_KERNEL].store(ver == 7 ? LF_KERNEL_TILE : 0);
     if (const char* e = getenv("LF_QTILE"))
       g_env_qtile = !strcmp(e, "blocks") ? 1 : !strcmp(e, "paired") ? 2 : *e ? 0 : -1;
     g_opt[LF_OPT_QTILE].store(-1);
@@ -257,14 +243,14 @@ int launch_pool(PoolArgs& a, int dtype, int vec, int ns, cudaStream_t st) {
 // forced attention kernel (LF_OPT_ATTN_KERNEL, for experiments), 0 = per call
 int forced_kernel() {
   const int v = opt(LF_OPT_ATTN_KERNEL);
-  return v == LF_KERNEL_PAIR || v == LF_KERNEL_TILE ? v : 0;
+  return v == LF_KERNEL_TILE ? v : 0;
 }
 
-// Kernel choice.  The tile kernel with two softmax sets (v7) matches or beats
-// the pair kernel (v5) at every measured shape (B200: c2 1025 vs 907 TFLOP/s,
-// c3 576 vs 549, c5_s50 524 vs 480, c4 1041 vs 1043, c5_dense 1051 vs 1047)
-// without stream-K merges, so LF_KERNEL_AUTO takes it; the pair kernel stays
-// available explicitly (LF_KERNEL_PAIR).
+// Kernel choice.  The tile kernel with two softmax sets (v7) matched or beat
+// the round-1 pair kernel (v5: two query tiles per CTA sharing K/V, stream-K
+// tail) at every measured shape (B200: c2 1025 vs 907 TFLOP/s, c3 576 vs 549,
+// c5_s50 524 vs 480, c4 1041 vs 1043, c5_dense 1051 vs 1047), so the pair
+// kernel was removed in round 2 (DESIGN.md §4 history).
 int choose_kernel(int heads, int n_qtiles, int dense_keys, int past_tiles, int sms) {
   (void)heads; (void)n_qtiles; (void)dense_keys; (void)past_tiles; (void)sms;
   return LF_KERNEL_TILE;
@@ -428,7 +414,6 @@ size_t tile_scratch_bytes(int d, int sms) {
   return kScratchCounterBytes + align_up((size_t)sms * 128 * 8, 256) + (size_t)sms * 128 * d * 4;
 }
 
-// v5: query-tile pairs; whole items round-robin, the tail (< grid items) stream-K
 // benchmarking probes: LF_ATTN_DEBUG=1 skips the softmax arithmetic; =2 records the
 // clock64 event trace of CTA LF_ATTN_TRACE_CTA (kernels built with the trace macro)
 // and writes it to gpurun_out/attn_trace.txt after the fourth launch
@@ -454,43 +439,6 @@ void setup_trace(AttnParams& p, void* stream) {
       }
     }
   }
-}
-
-int launch_v5(AttnParams& p, int heads, int d, int sms, const Scratch* scratch, void* stream) {
-  const int n_pairs = (p.n_qtiles + 1) / 2;
-  const int items = n_pairs * heads;
-  const int G = sms < AttnCfg5<128>::MAX_TAIL ? sms : AttnCfg5<128>::MAX_TAIL;
-  p.full_items = items / G * G;
-  const int R = items - p.full_items;
-  p.tail_split = 1;
-  p.part_o = nullptr;
-  p.part_ml = nullptr;
-  p.counters = nullptr;
-  if (R > 0) {
-    const size_t need_c = align_up((size_t)G * 4, 256);
-    const size_t need_ml = align_up((size_t)2 * G * 256 * 8, 256);
-    const size_t need_o = (size_t)2 * G * 256 * d * 4;
-    if (!launch_scratch(scratch, need_c, need_ml, need_o, S(stream), &p.counters, &p.part_ml,
-                        &p.part_o)) {
-      p.counters = nullptr;
-      p.part_ml = nullptr;
-      p.part_o = nullptr;  // kernel falls back to whole tail items
-    }
-  }
-  const int grid = items < G && !p.part_o ? items : G;
-  if (grid <= 0) return LF_OK;
-  setup_trace(p, stream);
-  const int poly = opt(LF_OPT_ATTN_POLY) > 0 ? opt(LF_OPT_ATTN_POLY) : 0;
-#define LF_V5(DD, PV)                                                                            \
-  if (d == DD && poly == PV) {                                                                \
-    cudaFuncSetAttribute(attn_fwd_v5_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         AttnCfg5<DD>::SMEM);                                                 \
-    attn_fwd_v5_kernel<DD, PV><<<grid, 384, AttnCfg5<DD>::SMEM, S(stream)>>>(p, items, n_pairs); \
-    return check_launch("attn_fwd_v5_kernel");                                               \
-  }
-  LF_V5(128, 0) LF_V5(64, 0) LF_V5(128, 4) LF_V5(128, 8) LF_V5(128, 3) LF_V5(128, 2)
-#undef LF_V5
-  return fail(LF_ERR_UNSUPPORTED, "attn_fwd_v5: d=%d poly=%d not instantiated", d, poly);
 }
 
 // tile kernel (v7): one query tile per CTA, split-KV of the last partial round
@@ -1128,16 +1076,9 @@ int lf_attention_paired(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_ti
   caller.bytes = scratch_bytes;
   const Scratch* cs = scratch ? &caller : nullptr;
   p.plan_pairs = plan_rows() != kTileRows;
-  if (kernel != LF_KERNEL_TILE && kernel != LF_KERNEL_PAIR)
-    kernel = choose_kernel(q->heads, p.n_qtiles, dense_hi > dense_lo ? dense_hi - dense_lo : 0,
-                           past_tiles_hint, sms);
-  if (forced_kernel()) kernel = forced_kernel();
-  if (p.qmode) kernel = LF_KERNEL_TILE;  // the pair kernel has 128-row tiles only
-  if (kernel == LF_KERNEL_PAIR) {
-    p.tma_out = out_dtype == LF_BF16 &&
-                make_out_map(&p.to, out, q->d, q->rows, q->heads, out_row_stride, out_head_stride);
-    return launch_v5(p, q->heads, q->d, sms, cs, stream);
-  }
+  if (kernel != LF_KERNEL_AUTO && kernel != LF_KERNEL_TILE)
+    return fail(LF_ERR_INVALID, "attention kernel %d: LF_KERNEL_AUTO or LF_KERNEL_TILE", kernel);
+  (void)past_tiles_hint;
   return launch_tile(p, q->heads, q->d, sms, cs, stream);
 }
 

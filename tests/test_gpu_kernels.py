@@ -1,8 +1,7 @@
-"""Both attention kernels, forced: the one-tile-per-CTA kernel with two softmax
-sets (LF_KERNEL_TILE, with its split-KV tail) and the query-tile-pair kernel
-with its stream-K split/merge tail (LF_KERNEL_PAIR), against the oracle on the
-same inputs (masks bit-exact, outputs within the tolerance of
-test_gpu_parity.py)."""
+"""The attention kernel forced (LF_KERNEL_TILE: one query tile per CTA, two
+softmax sets, split-KV tail) against the oracle on the same inputs (masks
+bit-exact, outputs within the tolerance of test_gpu_parity.py), its bf16
+epilogue and graph-replay determinism, and the kernel-choice ABI."""
 
 import numpy as np
 import pytest
@@ -13,7 +12,7 @@ from tests.test_gpu_parity import assert_close_attn
 
 pytestmark = pytest.mark.gpu
 
-TILE, PAIR = 3, 5
+TILE = 3
 
 
 @pytest.fixture(scope="module")
@@ -36,7 +35,7 @@ def _run(lf, kernel, H, n, f, i, d, s_i, topk, seed, out_dtype=torch.float32, he
     return pipe, out, (q, k, v)
 
 
-@pytest.mark.parametrize("kernel", [TILE, PAIR])
+@pytest.mark.parametrize("kernel", [TILE])
 @pytest.mark.parametrize("H,i,s_i,topk", [(12, 7, 0.5, 6), (3, 14, 0.8, 6), (1, 5, 0.0, 12),
                                           (2, 3, 0.3, 2)])
 def test_kernel_vs_oracle(lf, kernel, H, i, s_i, topk):
@@ -53,7 +52,7 @@ def test_kernel_vs_oracle(lf, kernel, H, i, s_i, topk):
         assert_close_attn(out[h], ref, f"kernel {kernel} head {h}")
 
 
-@pytest.mark.parametrize("kernel", [TILE, PAIR])
+@pytest.mark.parametrize("kernel", [TILE])
 @pytest.mark.parametrize("n,f,i,d,s_i,topk", [(256, 2, 3, 64, 0.3, 2), (1536, 3, 5, 128, 0.6, 3),
                                                (100, 1, 4, 64, 0.2, 2)])
 def test_kernel_small_shapes(lf, kernel, n, f, i, d, s_i, topk):
@@ -71,17 +70,17 @@ def test_kernel_small_shapes(lf, kernel, n, f, i, d, s_i, topk):
 
 
 @pytest.mark.parametrize("H", [12, 2])
-def test_pair_bf16_epilogue_matches_fp32(lf, H):
-    # bf16 output goes through the TMA-store epilogue (and, for H = 2, the
-    # split-merge path); it must equal the fp32 output rounded to bf16
-    _, o32, _ = _run(lf, PAIR, H, 1560, 3, 7, 128, 0.5, 6, seed=31)
-    _, o16, _ = _run(lf, PAIR, H, 1560, 3, 7, 128, 0.5, 6, seed=31, out_dtype=torch.bfloat16)
+def test_bf16_epilogue_matches_fp32(lf, H):
+    # bf16 output (and, for H = 2, the split-KV merge path) equals the fp32
+    # output rounded to bf16
+    _, o32, _ = _run(lf, TILE, H, 1560, 3, 7, 128, 0.5, 6, seed=31)
+    _, o16, _ = _run(lf, TILE, H, 1560, 3, 7, 128, 0.5, 6, seed=31, out_dtype=torch.bfloat16)
     assert torch.equal(o32.to(torch.bfloat16), o16)
 
 
-def test_pair_graph_replay_deterministic(lf):
-    # stream-K merges: whichever part finishes last merges, the result is bitwise stable
-    pipe, out, _ = _run(lf, PAIR, 4, 1560, 3, 5, 128, 0.5, 6, seed=5, out_dtype=torch.bfloat16)
+def test_split_graph_replay_deterministic(lf):
+    # split-KV tail merges: whichever part finishes last merges, the result is bitwise stable
+    pipe, out, _ = _run(lf, TILE, 4, 1560, 3, 5, 128, 0.5, 6, seed=5, out_dtype=torch.bfloat16)
     first = out.clone()
     pipe.capture()
     for _ in range(4):
@@ -96,6 +95,9 @@ def test_kernel_choice_is_reported(lf):
     # the two-softmax-set tile kernel is the automatic choice at every shape
     for args in ((12, 4680, 4680, 0), (40, 4680, 4680, 0), (12, 4680, 4680, 226)):
         assert lib.lf_attention_kernel_choice(*args) == TILE
+    # round 1's pair kernel (5) is gone: an explicit request for it is rejected
+    with pytest.raises(Exception, match="attention kernel 5"):
+        _run(lf, 5, 2, 256, 2, 3, 64, 0.3, 2, seed=3)
 
 
 @pytest.mark.parametrize("i,s_i,topk", [(7, 0.5, 6), (14, 0.8, 6), (5, 0.0, 12)])
