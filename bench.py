@@ -628,7 +628,8 @@ def run_ours(args, c):
     e2e_steps = max(3, min(args.steps, 20))
 
     def timed(fn, reps):
-        fn()
+        for _ in range(max(args.warmup, 3)):  # the same W >= 3 warm-up steps as the headline
+            fn()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
