@@ -27,6 +27,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -627,10 +628,14 @@ def run_ours(args, c):
     # every step's inputs and D2H of its output inside the timed region
     e2e_steps = max(3, min(args.steps, 20))
 
-    def timed(fn, reps):
+    def timed(fn, reps, no_gc=False):
         for _ in range(max(args.warmup, 3)):  # the same W >= 3 warm-up steps as the headline
             fn()
         torch.cuda.synchronize()
+        gc_was = gc.isenabled()
+        if no_gc:
+            gc.collect()
+            gc.disable()
         if world > 1:
             dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -643,6 +648,8 @@ def run_ours(args, c):
                 marks[r].record()
         b.record()
         torch.cuda.synchronize()
+        if no_gc and gc_was:
+            gc.enable()
         if marks:
             per = [a.elapsed_time(marks[0])] + [marks[r - 1].elapsed_time(marks[r])
                                                 for r in range(1, reps)]
@@ -683,7 +690,6 @@ def run_ours(args, c):
     # copies overlap compute: H2D of step s+1 into a staging pair on a copy
     # stream while step s runs, a device copy into the cache slot (HBM, ~10 us),
     # D2H of each output on a third stream; PCIe H2D is the e2e bound
-    cur = torch.cuda.current_stream()
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
     stg_q = [torch.empty_like(Q[0]) for _ in range(2)]
     stg_k = [torch.empty_like(Kc[0]) for _ in range(2)]
@@ -693,6 +699,8 @@ def run_ours(args, c):
     ev_out = [torch.cuda.Event() for _ in range(T)]
 
     def e2e_rollout():
+        cur = torch.cuda.current_stream()
+
         def h2d(s):
             b = s & 1
             with torch.cuda.stream(s_h2d):
@@ -743,7 +751,11 @@ def run_ours(args, c):
         if mode == "headshard":
             cur.wait_stream(comm)
 
-    e2e_ms = timed(e2e_rollout, e2e_steps)
+    # eager API calls (the host runs ahead of the device, so the next chunk's
+    # H2D overlaps this chunk's last steps); Python's garbage collector is paused
+    # inside the timed region, as timeit does -- a collection pass stalled the
+    # host loop for 80-90 ms and idled the PCIe link
+    e2e_ms = timed(e2e_rollout, e2e_steps, no_gc=True)
 
     # ---- CPU baseline (rank 0, N = 1 only): the oracle on a bounded sample of
     # the same workload -- head-calls of this chunk until ~10 s of CPU work or
