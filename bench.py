@@ -676,7 +676,7 @@ def run_ours(args, c):
             gather(s)
             ho[s].copy_(outs[s], non_blocking=True)
 
-    e2e_ms_sl = timed(e2e_stateless, e2e_steps)
+    e2e_ms_sl = timed(e2e_stateless, e2e_steps, no_gc=True)
 
     # (b) rollout driver (HsaRollout): per chunk the previous clean chunk's K/V
     # (commit) and, per denoising step, the current chunk's q, k, v
