@@ -37,7 +37,7 @@ struct AttnParams {
   // Parts write unnormalised partials; the last one to finish merges them.
   int full_items, tail_split;
   int debug;  // benchmarking probe: 1 = skip softmax arithmetic (P left as S bits), 2 = trace
-  long long* trace;  // debug == 2: clock64 event trace of CTA 0 (v5)
+  long long* trace;  // debug == 2: clock64 event trace of one CTA
   int plan_pairs;    // segs are 256-row (pair) plans
   int qmode;         // query-tile geometry (qtile_rows in common.cuh); 1, 2 imply plan_pairs
   const int* qperm;  // geometry 2: [H][2 * n_qtiles] query block of each 64-row tile half

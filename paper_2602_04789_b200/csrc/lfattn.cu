@@ -1045,8 +1045,7 @@ int lf_attention_paired(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_ti
   if (max_qblocks(q_tiling) > 32)
     return fail(LF_ERR_UNSUPPORTED, "more than 32 query blocks per plan tile");
   if (!out) return fail(LF_ERR_INVALID, "null out");
-  AttnParams p;
-  memset(&p, 0, sizeof(p));
+  AttnParams p{};
   if ((rc = make_map(&p.tq, q, 128)) || (rc = make_map(&p.tq2, q, 64)) ||
       (rc = make_map(&p.tk, k, 64)) || (rc = make_map(&p.tv, v, 64)))
     return rc;
@@ -1083,7 +1082,7 @@ int lf_attention_paired(const lf_mat* q, const lf_mat* k, const lf_mat* v, lf_ti
 }
 
 size_t lf_hsa_workspace_bytes(const lf_hsa_args* a) {
-  HsaGeom g;
+  HsaGeom g{};
   if (!a) return 0;
   QmodeScope qs = hsa_qmode_scope(a);
   if (hsa_geom(a, &g)) return 0;
@@ -1093,7 +1092,7 @@ size_t lf_hsa_workspace_bytes(const lf_hsa_args* a) {
 int lf_hsa_views(const lf_hsa_args* a, void* workspace, float** q_block, float** k_block,
                  float** k_frame, int32_t** blocks, int32_t** count, int32_t** frames,
                  int32_t** budget, int32_t* cap, int32_t* frame_cap) {
-  HsaGeom g;
+  HsaGeom g{};
   int rc;
   if (!a) return fail(LF_ERR_INVALID, "null args");
   QmodeScope qs = hsa_qmode_scope(a);
@@ -1112,7 +1111,7 @@ int lf_hsa_views(const lf_hsa_args* a, void* workspace, float** q_block, float**
 }
 
 int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes, void* stream) {
-  HsaGeom g;
+  HsaGeom g{};
   int rc;
   if (!a) return fail(LF_ERR_INVALID, "null args");
   QmodeScope qs = hsa_qmode_scope(a);

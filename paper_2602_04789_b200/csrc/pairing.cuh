@@ -57,13 +57,13 @@ struct PairArgs {
 
 __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) {
   extern __shared__ __align__(16) unsigned int pr_smem[];
-  const int h = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = blockIdx.x, tid = threadIdx.x;
 #ifdef LF_PAIR_TRACE
   long long tr[5];
   tr[0] = clock64();
   int rounds = 0;
 #endif
-  constexpr int NT = kPairThreads, NW = kPairThreads / 32;
+  constexpr int NT = kPairThreads;
   const int n = a.nqb, W = a.words;
   unsigned int* bits = pr_smem;                                          // [n][W]
   unsigned short* ov = reinterpret_cast<unsigned short*>(bits + n * W);  // [n][n]
