@@ -163,19 +163,16 @@ __device__ void emit_plan_segments(const unsigned int* qm, int list_blocks, cons
       pieces = (e - s + kSegKeys - 1) / kSegKeys;
     }
   };
-  // counting pass
+  // counting pass (most key blocks of a tile are unselected: empty 32-block
+  // chunks cost one ballot)
   int my[4] = {0, 0, 0, 0};
   for (int b0 = bw0; b0 < bw1; b0 += 32) {
     unsigned int m;
     int c, s, e, pieces;
     classify(b0 + lane, m, c, s, e, pieces);
+    if (!__ballot_sync(0xffffffffu, c != 0)) continue;
 #pragma unroll
-    for (int k = 1; k <= 3; ++k) {
-      int v = c == k ? pieces : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      my[k] += v;
-    }
+    for (int k = 1; k <= 3; ++k) my[k] += __reduce_add_sync(0xffffffffu, c == k ? pieces : 0);
   }
   if (lane == 0)
     for (int k = 1; k <= 3; ++k) cnt[warp][k] = my[k];
@@ -203,14 +200,21 @@ __device__ void emit_plan_segments(const unsigned int* qm, int list_blocks, cons
     unsigned int m;
     int c, s, e, pieces;
     classify(b0 + lane, m, c, s, e, pieces);
+    if (!__ballot_sync(0xffffffffu, c != 0)) continue;
+    const bool single = __reduce_max_sync(0xffffffffu, (unsigned)pieces) <= 1u;
 #pragma unroll
     for (int k = 1; k <= 3; ++k) {
       const int v = c == k ? pieces : 0;
-      int incl = v;
+      int incl;
+      if (single) {  // one piece per block (blocks <= 64 keys): ballot prefix
+        incl = __popc(__ballot_sync(0xffffffffu, v != 0) & (0xffffffffu >> (31 - lane)));
+      } else {
+        incl = v;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
       }
       if (v) {
         const int off = run[k] + incl - v;
@@ -316,10 +320,16 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   const int nq = qb1 - qb0 + 1 < 32 ? qb1 - qb0 + 1 : 32;
   if (tid < 32) s_qbs[tid] = tid < nq ? qb0 + tid : -1;
   __syncthreads();
+#ifdef LF_PLAN_TRACE
+  const long long t0 = clock64();
+#endif
   if (!gather_lists(a, h, s_qbs, nq, qm, s_off)) {
     if (tid == 0) a.seg_count[w] = 0;
     return;
   }
+#ifdef LF_PLAN_TRACE
+  const long long t1 = clock64();
+#endif
   auto bits = [&](int r0, int r1) -> unsigned int {
     if (r0 >= r1) return 0u;
     int lo = a.qt.block_of(r0) - qb0, hi = a.qt.block_of(r1 - 1) - qb0;
@@ -332,6 +342,12 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   const unsigned int maskB = pairs ? bits(mid, q1) : 0u;
   emit_plan_segments<4>(qm, a.list_blocks, a.kt, maskA, maskB, pairs,
                         a.segs + (size_t)w * a.seg_cap, a.seg_cap, a.seg_count + w, cnt);
+#ifdef LF_PLAN_TRACE
+  const long long t2 = clock64();
+  if (tid == 0 && (w == 0 || w == (int)gridDim.x / 2))
+    printf("plan_trace cta %d: gather %lld emit %lld (list blocks %d)\n", w, t1 - t0, t2 - t1,
+           a.list_blocks);
+#endif
 }
 
 }  // namespace lf
