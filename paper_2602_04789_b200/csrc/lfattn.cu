@@ -823,7 +823,8 @@ static int select_launch(const float* q_block, const float* k_block, int64_t kb_
                          const double* s_i_dev, int32_t cap, int32_t frame_cap,
                          int32_t* out_blocks, int32_t* out_count, int32_t* out_frames,
                          double* out_scores, double* out_fscores, int32_t* out_budget,
-                         double* out_margin, void* stream) {
+                         double* out_margin, void* stream, unsigned int* out_bits = nullptr,
+                         int bits_words = 0) {
   if (!q_block || !k_block || !s_i_dev || !out_blocks || !out_count || !out_frames)
     return fail(LF_ERR_INVALID, "lf_select: null pointer");
   if (heads < 1 || nqb < 1 || d < 1 || blocks_per_frame < 1 || chunk_index < 1 || frames_per_chunk < 1)
@@ -840,7 +841,8 @@ static int select_launch(const float* q_block, const float* k_block, int64_t kb_
             frames_per_chunk, topk_frames, per_frame_mode ? 1 : 0, s_i_dev, cap, frame_cap,
             out_blocks, out_count, out_frames, out_scores, out_fscores, out_budget, max_cand,
             (long long)kb_head_stride, (long long)kf_head_stride, out_margin,
-            opt(LF_OPT_SELECT_EXACT) == 1 ? 1 : 0, screen_gamma(d)};
+            opt(LF_OPT_SELECT_EXACT) == 1 ? 1 : 0, screen_gamma(d),
+            bits_words > 0 && bits_words <= 64 ? out_bits : nullptr, bits_words};
   // one 4-warp CTA per (head, query block)
   if (lay.bytes > 48 * 1024)
     cudaFuncSetAttribute(select_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.bytes);
@@ -896,21 +898,30 @@ int lf_plan_tiles(const int32_t* blocks, const int32_t* count, int32_t heads, in
                               seg_cap, segs, seg_count, nullptr, stream);
 }
 
-int lf_pair_qblocks(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
-                    int32_t cap, int32_t list_blocks, int32_t* qperm, void* stream) {
+// bitset row length of the pairing (odd: conflict-free reads of consecutive rows)
+static int pair_words(int list_blocks) { return (((list_blocks > 0 ? list_blocks : 0) + 31) / 32) | 1; }
+
+static int pair_launch(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                       int32_t cap, int32_t list_blocks, int32_t* qperm,
+                       const unsigned int* bits_in, void* stream) {
   if (!qperm || !blocks || !count || heads < 1 || nqb < 1 || cap < 1)
     return fail(LF_ERR_INVALID, "lf_pair_qblocks: bad args");
   const int lb = list_blocks > 0 ? list_blocks : 0;
-  const int words = ((lb + 31) / 32) | 1;  // odd row stride: conflict-free lane-per-row reads
+  const int words = pair_words(lb);
   const size_t smem = (size_t)nqb * words * 4 + align_up((size_t)nqb * nqb * 2, 4) + nqb * 12 + 4;
   if (smem > 200 * 1024 || nqb > 1000)
     return fail(LF_ERR_UNSUPPORTED, "pairing working set too large");
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(pair_qblocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  PairArgs a{blocks, count, nqb, cap, lb, words, qperm};
+  PairArgs a{blocks, count, nqb, cap, lb, words, qperm, bits_in};
   pair_qblocks_kernel<<<heads, kPairThreads, smem, S(stream)>>>(a);
   return check_launch("pair_qblocks_kernel");
+}
+
+int lf_pair_qblocks(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
+                    int32_t cap, int32_t list_blocks, int32_t* qperm, void* stream) {
+  return pair_launch(blocks, count, heads, nqb, cap, list_blocks, qperm, nullptr, stream);
 }
 
 int lf_plan_tiles_paired(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
@@ -968,13 +979,23 @@ int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_s
   const bool paired = qmode_for(q_tiling) == 2;
   if (paired && !qperm)
     return fail(LF_ERR_INVALID, "paired query tiles need a qperm output (lf_pair_qblocks)");
+  // geometry 2: the selection also writes each query block's selection as a
+  // bitset, into the segment buffer (the plan overwrites it only after the
+  // pairing has read it), so the pairing needs no gather of the lists
+  unsigned int* bits = nullptr;
+  const int words = pair_words(list_blocks);
+  if (paired && segs && words <= 64 &&
+      (size_t)heads * nqb * words * 4 <=
+          (size_t)heads * plan_tile_count(q_tiling) * (seg_cap > 0 ? seg_cap : 0) * 16)
+    bits = reinterpret_cast<unsigned int*>(segs);
   if ((rc = select_launch(q_block, k_block, kb_head_stride, k_frame, kf_head_stride, heads, nqb,
                           nkb, d, blocks_per_frame, chunk_index, frames_per_chunk, topk_frames,
                           per_frame_mode, s_i_dev, cap, frame_cap, out_blocks, out_count,
-                          out_frames, nullptr, nullptr, out_budget, out_margin, stream)))
+                          out_frames, nullptr, nullptr, out_budget, out_margin, stream, bits,
+                          bits ? words : 0)))
     return rc;
-  if (paired && (rc = lf_pair_qblocks(out_blocks, out_count, heads, nqb, cap, list_blocks, qperm,
-                                      stream)))
+  if (paired && (rc = pair_launch(out_blocks, out_count, heads, nqb, cap, list_blocks, qperm,
+                                  bits, stream)))
     return rc;
   return lf_plan_tiles_paired(out_blocks, out_count, heads, nqb, cap, q_tiling, k_tiling,
                               list_blocks, seg_cap, segs, seg_count, paired ? qperm : nullptr,

@@ -53,6 +53,7 @@ struct PairArgs {
   const int* count;   // [H][nqb]
   int nqb, cap, list_blocks, words;
   int* qperm;         // [H][2 * ceil(nqb / 2)]
+  const unsigned int* bits_in;  // optional [H][nqb][words]: the bitsets, written by the selection
 };
 
 __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) {
@@ -71,9 +72,19 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
   int* mate = prop + n;                                                  // [n] (-1 unpaired)
   __shared__ int s_new;
   int* cnt = mate + n;  // [n] selection counts
-  for (int i = tid; i < n * W; i += NT) bits[i] = 0u;
+  if (!a.bits_in)
+    for (int i = tid; i < n * W; i += NT) bits[i] = 0u;
   int any = 0;
-  for (int i = tid; i < n; i += NT) {
+  if (a.bits_in) {  // bitsets from the selection kernel: one coalesced copy
+    for (int i = tid; i < n; i += NT) mate[i] = -1;
+    const unsigned int* src = a.bits_in + (size_t)h * n * W;
+    for (int i = tid; i < n * W; i += NT) {
+      const unsigned int v = __ldg(src + i);
+      bits[i] = v;
+      any |= v != 0u;
+    }
+  }
+  for (int i = tid; !a.bits_in && i < n; i += NT) {
     mate[i] = -1;
     const int c = __ldg(a.count + (size_t)h * n + i);
     cnt[i] = c < a.cap ? c : a.cap;
@@ -84,7 +95,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
   // rows (different words: no atomic conflicts), R-strided entries per thread
   const int* lst = a.blocks + (size_t)h * n * a.cap;
   const int R = n < NT ? NT / n : 1;
-  for (int task = tid; task < n * R; task += NT) {
+  for (int task = tid; !a.bits_in && task < n * R; task += NT) {
     const int x = task % n, k = task / n, c = cnt[x];
     const int* row = lst + (size_t)x * a.cap;
 #pragma unroll 4

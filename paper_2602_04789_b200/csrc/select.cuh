@@ -63,6 +63,8 @@ struct SelArgs {
   double* out_margin;  // optional [H][nqb][2] top-k margin certificate
   int exact;           // 1: exact scores for every list (no screening)
   float gamma;         // screen_gamma(d)
+  unsigned int* out_bits;  // optional [H][nqb][bits_words]: bitset of the selected past blocks
+  int bits_words;          // <= 64 (the pairing kernel reads these instead of the lists)
 };
 
 // shared-memory layout of select_screen_kernel (host and device)
@@ -680,7 +682,10 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
 
   const int C = nsel * bpf;
   double* om = a.out_margin ? a.out_margin + 2 * ((size_t)h * a.nqb + r) : nullptr;
+  unsigned int* obits = a.out_bits ? a.out_bits + ((size_t)h * a.nqb + r) * a.bits_words : nullptr;
   if (C == 0 || past_budget == 0) {
+    if (obits)
+      for (int e = tid; e < a.bits_words; e += kSelThreads) obits[e] = 0u;
     if (tid == 0) {
       a.out_count[w] = 0;
       if (om) {
@@ -720,6 +725,18 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
   if (om && tid == 0) {
     om[0] = margin_f;
     om[1] = margin_b;
+  }
+  if (obits) {  // the selection as a bitset over the past blocks (pairing input)
+    __shared__ unsigned int s_bits[64];
+    for (int e = tid; e < a.bits_words; e += kSelThreads) s_bits[e] = 0u;
+    __syncthreads();
+    for (int c = tid; c < C; c += kSelThreads)
+      if (flag[c]) {
+        const int fi = c / bpf, b = fsel[fi] * bpf + (c - fi * bpf);
+        atomicOr(&s_bits[b >> 5], 1u << (b & 31));
+      }
+    __syncthreads();
+    for (int e = tid; e < a.bits_words; e += kSelThreads) obits[e] = s_bits[e];
   }
   if (tid < 32) {
     int cnt = 0;

@@ -54,6 +54,36 @@ def test_pairing_is_a_deterministic_permutation(lf):
     assert (3, 40) in pairs
 
 
+@pytest.mark.parametrize("chunk,s_i", [(7, 0.5), (7, 0.7), (14, 0.8)])
+def test_select_plan_bitsets_pair_like_the_lists(lf, chunk, s_i):
+    """lf_select_plan under geometry 2 pairs from the bitsets the selection
+    kernel writes (staged in the segment buffer); lf_pair_qblocks gathers the
+    lists.  Same pairing, and the plans built from it agree."""
+    from paper_2602_04789_b200 import device as D
+    H, f, n, d, topk = 3, 3, 1560, 128, 6
+    bpf = -(-n // 64)
+    qt = D.TilingSpec(f * n, n, 64)
+    kt = D.TilingSpec(chunk * f * n, n, 64)
+    P = (chunk - 1) * f
+    g = torch.Generator(device="cuda").manual_seed(chunk)
+    qb = torch.randn((H, qt.count, d), device="cuda", generator=g) * 0.125
+    kb = torch.randn((H, kt.count, d), device="cuda", generator=g) * 0.125
+    kf = torch.randn((H, P, d), device="cuda", generator=g) * 0.05
+    with D.qtile_scope(2):
+        sel, tiles, _ = D.select_plan(qb, kb, kf, bpf, chunk, f, topk, False, s_i, qt, kt,
+                                      P * bpf)
+        ref = D.pair_qblocks(sel.blocks, sel.count, P * bpf)
+        ref_tiles = D.plan_tiles(sel.blocks, sel.count, qt, kt, P * bpf, qperm=ref)
+    torch.cuda.synchronize()
+    assert torch.equal(tiles.qperm, ref)
+    assert torch.equal(tiles.seg_count, ref_tiles.seg_count)
+    sc = tiles.seg_count.cpu().numpy()
+    a_, b_ = tiles.segs.cpu().numpy(), ref_tiles.segs.cpu().numpy()
+    for h in range(H):
+        for t in range(sc.shape[1]):
+            np.testing.assert_array_equal(a_[h, t, :sc[h, t]], b_[h, t, :sc[h, t]])
+
+
 @pytest.mark.parametrize("i,s_i,topk,H", [(7, 0.5, 6, 3), (7, 0.7, 6, 2), (14, 0.8, 6, 2),
                                           (4, 0.3, 3, 2)])
 def test_pipeline_paired_vs_oracle(lf, lfopt, i, s_i, topk, H):
