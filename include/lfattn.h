@@ -309,7 +309,12 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
 #define LF_OPT_ATTN_KERNEL 8  /* LF_ATTN_VER (7): forced attention kernel, 0 auto      */
 #define LF_OPT_QTILE 9        /* LF_QTILE (blocks|paired|rows) / lf_set_qtile_mode    */
 #define LF_OPT_TRACE_CTA 10   /* LF_ATTN_TRACE_CTA                                   */
-#define LF_OPT_COUNT 11
+#define LF_OPT_PDL 11         /* LF_PDL: 1 (default) = the step kernels (query pool,
+                                 select, pair, plan, attention) launch as programmatic
+                                 dependents of the previous kernel on the stream; each
+                                 waits for it (griddepcontrol.wait) before touching
+                                 memory, so only the launch latency overlaps; 0 = off */
+#define LF_OPT_COUNT 12
 int lf_set_option(int32_t opt, int32_t value); /* LF_ERR_INVALID for an unknown opt */
 int lf_get_option(int32_t opt);                /* -2 for an unknown opt             */
 

@@ -40,7 +40,7 @@ EXPORTS = (
 OPTIONS = {
     "pool_cfg": 0, "pool_no_tma": 1, "attn_split": 2, "attn_sched": 3, "plan_warp": 4,
     "select_exact": 5, "attn_debug": 6, "attn_poly": 7, "attn_kernel": 8, "qtile": 9,
-    "trace_cta": 10,
+    "trace_cta": 10, "pdl": 11,
 }
 
 

@@ -39,12 +39,25 @@ struct AttnCfg7 {
 #endif
   static constexpr int KST = LF_V7_KST;  // K ring stages
   static constexpr int VST = LF_V7_VST;  // V ring stages
+#ifndef LF_V7_QST
+#define LF_V7_QST 1
+#endif
+  // Q buffers: with 2 the next item's Q is in shared memory before this
+  // item's last PV, so its first QK follows the drain without a load latency
+  // (fits beside K2/V3 with 512 bytes of alignment slack).  Measured neutral
+  // (c2 +0 %, c3 +0.5 %, c5_s50 -4 %, c5_s70 +1 %, c5_dense +1 %;
+  // profiles/r02/qst2_ab.txt), so one buffer stays the default
+  static constexpr int QST = LF_V7_QST;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_K = OFF_Q + QST * Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + VST * KV_BYTES;
   static constexpr int OFF_STAT = OFF_BAR + 512;  // float2 [2 sets][128 rows]
-  static constexpr int SMEM = OFF_STAT + 2 * 128 * 8 + 1024;
+  // alignment slack for the 1024-byte swizzle atoms: the dynamic window starts
+  // 1 KB-aligned on sm_100 (after the reserved 1 KB), so 512 bytes of slack
+  // suffice where 1024 would not fit; checked at run time
+  static constexpr int SLACK = (OFF_STAT + 2 * 128 * 8 + 1024 <= 232448) ? 1024 : 512;
+  static constexpr int SMEM = OFF_STAT + 2 * 128 * 8 + SLACK;
   static_assert(SMEM <= 232448, "shared memory");
   static constexpr int TMEM_COLS = 512;
   static constexpr int COL_S = 0;    // + 128 * set
@@ -70,7 +83,12 @@ __global__ void __launch_bounds__(320, 1)
     attn_fwd_v7_kernel(const __grid_constant__ AttnParams p, int total_work) {
   using C = AttnCfg7<D>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  if (pad > (uint32_t)C::SLACK) {  // uniform over the CTA: nothing initialised yet
+    if (threadIdx.x == 0 && p.err) atomicOr(p.err, 2);
+    return;
+  }
+  unsigned char* smem = smem_raw + pad;
   unsigned char* sQ = smem + C::OFF_Q;
   unsigned char* sK = smem + C::OFF_K;
   unsigned char* sV = smem + C::OFF_V;
@@ -87,7 +105,10 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* v_empty = bars + 22;  // [VST]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
   int* flag = reinterpret_cast<int*>(bars + 27);
-  static_assert(C::KST <= 4 && C::VST <= 4, "barrier slots");
+  static_assert(C::KST <= 4 && C::VST <= 4 && C::QST <= 2, "barrier slots");
+  // Q buffer b: full / empty at bars[0] / bars[1] (b = 0), bars[28] / bars[29] (b = 1)
+  auto qfull = [&](uint32_t b) { return b ? bars + 28 : q_full; };
+  auto qempty = [&](uint32_t b) { return b ? bars + 29 : q_empty; };
   // dynamic item schedule (p.sched): the producer warp fetches the next unit
   // from a global counter when it is ready for its Q and publishes the unit id
   // through a 4-slot ring to the MMA warp and the 8 softmax warps; null sched:
@@ -116,8 +137,10 @@ __global__ void __launch_bounds__(320, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int b = 0; b < C::QST; ++b) {
+      mbar_init(qfull(b), 1);
+      mbar_init(qempty(b), 1);
+    }
     for (int x = 0; x < 2; ++x) {
       mbar_init(s_full + x, 1);
       mbar_init(p_full + 2 * x, 128);
@@ -144,6 +167,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // set-up above overlapped the previous kernel; plans / outputs below
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA producer
@@ -176,15 +200,16 @@ __global__ void __launch_bounds__(320, 1)
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
       if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8, clk64());
-      mbar_wait(q_empty, (nq++ & 1) ^ 1);
+      const uint32_t qb = nq % C::QST;
+      mbar_wait(qempty(qb), ((nq++ / C::QST) & 1) ^ 1);
       if (elect_one()) {  // the tile's two 64-row halves (geometry 2: any two query blocks)
         const int halves = (cx.sz[0] > 0) + (cx.sz[1] > 0);
-        mbar_expect_tx(q_full, halves * (C::Q_BYTES / 2));
+        mbar_expect_tx(qfull(qb), halves * (C::Q_BYTES / 2));
         for (int hs = 0; hs < 2; ++hs) {
           if (cx.sz[hs] == 0) continue;  // rows never stored: stale shared memory is fine
           for (int a = 0; a < C::ATOMS; ++a)
-            tma_load_3d(&p.tq2, q_full, sQ + a * (C::BM * 128) + hs * (64 * 128), a * 64,
-                        cx.gs[hs], wi.h);
+            tma_load_3d(&p.tq2, qfull(qb), sQ + qb * C::Q_BYTES + a * (C::BM * 128) + hs * (64 * 128),
+                        a * 64, cx.gs[hs], wi.h);
         }
       }
       __syncwarp();
@@ -243,7 +268,7 @@ __global__ void __launch_bounds__(320, 1)
     // ------------------------------------------------------------- MMA issuer
     constexpr uint32_t IDESC_QK = idesc_bf16(128, 128, 0, 0);
     constexpr uint32_t IDESC_PV = idesc_bf16(128, D, 0, 1);
-    const uint64_t qd = smem_desc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t qd0 = smem_desc_sw128(smem_u32(sQ), 16, 1024);
     const uint64_t kd0 = smem_desc_sw128(smem_u32(sK), 16, 1024);
     const uint64_t vd0 = smem_desc_sw128(smem_u32(sV), C::BN * 128, 1024);
     uint32_t kit = 0, nq = 0, np[2] = {0, 0}, noe = 0;
@@ -253,7 +278,9 @@ __global__ void __launch_bounds__(320, 1)
       const WorkItem wi = work_item(p, w);
       const TileCtx cx = tile_ctx(p, wi);
       if (cx.j1 == cx.j0) continue;
-      mbar_wait(q_full, nq & 1);
+      const uint32_t qb = nq % C::QST;
+      mbar_wait(qfull(qb), (nq / C::QST) & 1);
+      const uint64_t qd = qd0 + ((uint32_t)(qb * C::Q_BYTES) >> 4);
       if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8 + 1, clk64());
       ++nq;
       int pend[2] = {-1, -1};
@@ -328,7 +355,7 @@ __global__ void __launch_bounds__(320, 1)
         if (pend[0] >= 0) issue_pv(0);
         if (pend[1] >= 0) issue_pv(1);
       }
-      tc_commit_elect(q_empty);
+      tc_commit_elect(qempty(qb));
       if (k > 0) tc_commit_elect(o_full);
     }
     __syncwarp();

@@ -95,6 +95,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Programmatic dependent launch (host: LF_OPT_PDL): wait until the previous
+// kernel on the stream has completed and its memory is visible, then allow the
+// next kernel to be scheduled.  A no-op for a kernel launched without the
+// attribute.  Called before a step kernel's first global access, so only the
+// launch latency (and CTA setup) overlaps the previous kernel's tail.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }

@@ -124,12 +124,34 @@ void init_options() {
       g_env_qtile = !strcmp(e, "blocks") ? 1 : !strcmp(e, "paired") ? 2 : *e ? 0 : -1;
     g_opt[LF_OPT_QTILE].store(-1);
     g_opt[LF_OPT_TRACE_CTA].store(env_int("LF_ATTN_TRACE_CTA", 0));
+    g_opt[LF_OPT_PDL].store(env_int("LF_PDL", 1));
   });
 }
 
 int opt(int i) {
   init_options();
   return g_opt[i].load(std::memory_order_relaxed);
+}
+
+// Launch of a step kernel (query pool, select, pair, plan, attention) as a
+// programmatic dependent of the previous kernel on the stream (LF_OPT_PDL):
+// its CTAs may be scheduled while that kernel drains and block in pdl_wait()
+// (common.cuh) until it has completed, so a dependent chain of short kernels
+// does not pay the full launch latency between links.
+template <typename... KArgs, typename... Args>
+void launch_step(void (*k)(KArgs...), int grid, int block, size_t smem, void* stream,
+                 Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = S(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = opt(LF_OPT_PDL) != 0 ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 // SM count of the current device (cached per device ordinal)
@@ -165,7 +187,7 @@ void launch_frame_pool_tma(const FramePoolArgs& fa, int d, int smem, int grid, v
     const int tsmem = PC::NST * PC::STAGE + PC::BAR_BYTES + smem;                         \
     cudaFuncSetAttribute(pool_frames_tma_kernel<D_, G_, N_>,                              \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);             \
-    pool_frames_tma_kernel<D_, G_, N_><<<grid, PC::THREADS, tsmem, S(stream)>>>(fa);      \
+    launch_step(pool_frames_tma_kernel<D_, G_, N_>, grid, PC::THREADS, tsmem, stream, fa); \
   } while (0)
   if (d == 128) {
     if (pcfg == 3) LF_POOL_LAUNCH(128, 8, 8);
@@ -489,7 +511,7 @@ int launch_tile(AttnParams& p, int heads, int d, int sms, const Scratch* scratch
   if (d == DD && poly == PV) {                                                                \
     cudaFuncSetAttribute(attn_fwd_v7_kernel<DD, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          AttnCfg7<DD>::SMEM);                                                 \
-    attn_fwd_v7_kernel<DD, PV><<<grid, 320, AttnCfg7<DD>::SMEM, S(stream)>>>(p, work);        \
+    launch_step(attn_fwd_v7_kernel<DD, PV>, grid, 320, AttnCfg7<DD>::SMEM, stream, p, work);  \
     return check_launch("attn_fwd_v7_kernel");                                               \
   }
   LF_V7(128, 0) LF_V7(64, 0) LF_V7(128, 4)
@@ -846,7 +868,7 @@ static int select_launch(const float* q_block, const float* k_block, int64_t kb_
   // one 4-warp CTA per (head, query block)
   if (lay.bytes > 48 * 1024)
     cudaFuncSetAttribute(select_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.bytes);
-  select_screen_kernel<<<heads * nqb, kSelThreads, lay.bytes, S(stream)>>>(a);
+  launch_step(select_screen_kernel, heads * nqb, kSelThreads, lay.bytes, stream, a);
   return check_launch("select_screen_kernel");
 }
 
@@ -915,7 +937,7 @@ static int pair_launch(const int32_t* blocks, const int32_t* count, int32_t head
     cudaFuncSetAttribute(pair_qblocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   PairArgs a{blocks, count, nqb, cap, lb, words, qperm, bits_in};
-  pair_qblocks_kernel<<<heads, kPairThreads, smem, S(stream)>>>(a);
+  launch_step(pair_qblocks_kernel, heads, kPairThreads, smem, stream, a);
   return check_launch("pair_qblocks_kernel");
 }
 
@@ -954,7 +976,7 @@ int lf_plan_tiles_paired(const int32_t* blocks, const int32_t* count, int32_t he
   if (qmode || opt(LF_OPT_PLAN_WARP) != 1) {  // the warp planner knows 128/256-row tiles only
     if (spw > 48 * 1024)
       cudaFuncSetAttribute(plan_tiles_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, spw);
-    plan_tiles_cta_kernel<<<heads * ntiles, 128, spw, S(stream)>>>(a);
+    launch_step(plan_tiles_cta_kernel, heads * ntiles, 128, spw, stream, a);
     return check_launch("plan_tiles_cta_kernel");
   }
   const int smem = wpc * spw;

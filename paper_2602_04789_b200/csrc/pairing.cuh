@@ -59,6 +59,7 @@ struct PairArgs {
 __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) {
   extern __shared__ __align__(16) unsigned int pr_smem[];
   const int h = blockIdx.x, tid = threadIdx.x;
+  pdl_wait();
 #ifdef LF_PAIR_TRACE
   long long tr[5];
   tr[0] = clock64();

@@ -305,6 +305,7 @@ template <int D, int G, int NSTAGES>
 __global__ void __launch_bounds__(PoolTmaCfg<D, G, NSTAGES>::THREADS) pool_frames_tma_kernel(FramePoolArgs a) {
   using C = PoolTmaCfg<D, G, NSTAGES>;
   extern __shared__ __align__(128) unsigned char pt_smem[];
+  pdl_wait();
   unsigned char* ring = pt_smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(pt_smem + C::NST * C::STAGE);
   uint64_t* empty = full + C::NST;

@@ -595,6 +595,7 @@ __device__ __noinline__ double list_margin(const double* x, const unsigned char*
 __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a) {
   extern __shared__ __align__(16) unsigned char sel_smem[];
   const int tid = threadIdx.x, lane = tid & 31;
+  pdl_wait();
   SEL_MARK(0);
   const int w = blockIdx.x;
   const int h = w / a.nqb, r = w - h * a.nqb;

@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(128) plan_tiles_cta_kernel(PlanArgs a) {
   __shared__ int cnt[4][4];  // [warp][class 1..3] (emit_plan_segments)
   __shared__ int s_qbs[32], s_off[33];
   const int tid = threadIdx.x;
+  pdl_wait();
   const int w = blockIdx.x;
   const int h = w / a.ntiles, t = w - h * a.ntiles;
   if (a.qmode == 2) {  // plan tile t = query tiles 2t, 2t+1 = query blocks qperm[4t .. 4t+3]
