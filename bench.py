@@ -351,10 +351,20 @@ def run_ours(args, c):
                                                 partition_heads)
 
     rank, world, local = dist_env()
+    # LF_BENCH_DIST_CHECK=1 (under torchrun): a functional check of the N-rank
+    # flow (head shards, eager gathers between step graphs, max-over-ranks
+    # timing, the JSON line) with every rank on the node's first GPUs and gloo
+    # for the collectives; not a measurement (the line says so)
+    dist_check = world > 1 and os.environ.get("LF_BENCH_DIST_CHECK") == "1"
+    if dist_check:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if dist_check:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     H, d, f, n, i, T = c["heads"], c["d"], c["f"], c["n"], c["chunk"], c["T"]
     lay = make_layout(lf, c)
     cfg = lf.SelectionConfig(topk_frames=c["topk"], block_budget_mode=c["mode"])
@@ -536,10 +546,30 @@ def run_ours(args, c):
     for _ in range(max(args.warmup, 3)):
         chunk_flow()
     torch.cuda.synchronize()
-    g_chunk = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_chunk):
-        chunk_flow()
-    g_chunk.replay()
+    if mode == "headshard" and flow == "serial":
+        # NCCL stays out of the graphs: one graph per step (compute only), the
+        # all-gather of step s launched eagerly on the comm stream after it
+        # (overlapping step s+1), so a rank never replays a captured collective
+        g_steps = []
+        for s in range(T):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                if s == 0 and i > 1:
+                    ro.commit(None, None, i - 1, overwrite=True)
+                ro.attend(ro.prepare(Q[s], i, s_i=s_dev, s_host=s_host), out=r_out[s])
+            g_steps.append(g)
+
+        def run_chunk():
+            for s in range(T):
+                g_steps[s].replay()
+                gather_heads_overlapped(r_out[s], shard, full[s], comm)
+            torch.cuda.current_stream().wait_stream(comm)
+    else:
+        g_chunk = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_chunk):
+            chunk_flow()
+        run_chunk = g_chunk.replay
+    run_chunk()
     torch.cuda.synchronize()
     fl = torch.tensor([float(flops_r)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -549,7 +579,7 @@ def run_ours(args, c):
     torch.cuda.synchronize()
     e0.record()
     for _ in range(args.steps):
-        g_chunk.replay()
+        run_chunk()
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -560,7 +590,7 @@ def run_ours(args, c):
     ms_chunk_r = float(t.item())
     clk = clocks.stop()
     if os.environ.get("LF_BENCH_TIMELINE") and rank == 0:
-        timeline_dump(lambda: g_chunk.replay(), os.environ["LF_BENCH_TIMELINE"])
+        timeline_dump(run_chunk, os.environ["LF_BENCH_TIMELINE"])
         timeline_dump(chunk_flow, os.environ["LF_BENCH_TIMELINE"] + ".eager.csv")
     value = flops_r_step / (ms_chunk_r * 1e-3) / 1e12
     errs += int(ro.err.item())
@@ -785,9 +815,6 @@ def run_ours(args, c):
             pl = ro.prepare(stg_q[b], i, s_i=s_dev, s_host=s_host)
             ro.attend(pl, out=r_out[s])
             ev_free[b].record(cur)
-            if mode == "headshard":
-                gather_heads_overlapped(r_out[s], shard, full[s], comm)
-                cur.wait_stream(comm)
             ev_out[s].record(cur)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev_out[s])
@@ -813,7 +840,14 @@ def run_ours(args, c):
     with torch.cuda.graph(g_e2e):
         e2e_chunk()
     torch.cuda.synchronize()
-    e2e_ms = timed(g_e2e.replay, e2e_steps, no_gc=True)
+
+    def e2e_replay():
+        g_e2e.replay()
+        if mode == "headshard":  # the chunk's all-gathers, eager (NCCL stays out of graphs)
+            for s in range(T):
+                gather_heads_overlapped(r_out[s], shard, full[s], comm)
+            torch.cuda.current_stream().wait_stream(comm)
+    e2e_ms = timed(e2e_replay, e2e_steps, no_gc=True)
 
     # ---- CPU baseline (rank 0, N = 1 only): the oracle on a bounded sample of
     # the same workload -- head-calls of this chunk until ~10 s of CPU work or
@@ -883,6 +917,8 @@ def run_ours(args, c):
             "ms_per_chunk": ms_chunk_r, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": job_config(args, c, s_host, world),
+            **({"dist_check": "functional check: all ranks on one GPU, gloo; not a measurement"}
+               if dist_check else {}),
             "query_tiles": {0: "128-row", 1: "block-aligned (2 query blocks)",
                             2: "2 query blocks paired by selection overlap"}.get(
                                 int(getattr(pl, "qmode", 0) or 0), "128-row"),

@@ -49,6 +49,10 @@ def gather_heads(local: torch.Tensor, shard: HeadShard, out: torch.Tensor | None
     backend = dist.get_backend(group)
     if backend == "nccl":
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    elif local.is_cuda:  # gloo with device tensors (functional checks): through host memory
+        parts = [torch.empty(local.shape, dtype=local.dtype) for _ in range(shard.world)]
+        dist.all_gather(parts, local.detach().cpu().contiguous(), group=group)
+        out.copy_(torch.cat(parts, dim=0))
     else:  # gloo (CPU tests): list form
         parts = list(out.split(shard.local_heads, dim=0))
         dist.all_gather(parts, local.contiguous(), group=group)
