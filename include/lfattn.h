@@ -87,7 +87,10 @@ int lf_compress(const lf_mat* q, const lf_mat* k, lf_tiling q_tiling, lf_tiling 
  *                  round_half_up((1-s_i)*chunk*current_blocks), chunk 1 -> 0 past.
  *   out_blocks     [H][nqb][cap] ascending absolute past block ids
  *   out_count      [H][nqb]
- *   out_frames     [H][nqb][frame_cap] ascending retrieved past frames (-1 pad)
+ *   out_frames     [H][nqb][frame_cap] ascending retrieved past frames (-1 pad);
+ *                  NULL = not wanted: then a call whose past budget is 0 (and
+ *                  that requests no scores / margins) skips the frame ranking,
+ *                  which cannot change the blocks (selection.py:154-155)
  *   out_scores     optional [H][nqb][cap] fp64 block scores (NULL to skip)
  *   out_fscores    optional [H][nqb][past_frames] fp64 frame scores
  *   out_budget     optional int32[3]: total, past budget, clamped flag        */

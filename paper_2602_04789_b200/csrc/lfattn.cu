@@ -847,7 +847,7 @@ static int select_launch(const float* q_block, const float* k_block, int64_t kb_
                          double* out_scores, double* out_fscores, int32_t* out_budget,
                          double* out_margin, void* stream, unsigned int* out_bits = nullptr,
                          int bits_words = 0) {
-  if (!q_block || !k_block || !s_i_dev || !out_blocks || !out_count || !out_frames)
+  if (!q_block || !k_block || !s_i_dev || !out_blocks || !out_count)
     return fail(LF_ERR_INVALID, "lf_select: null pointer");
   if (heads < 1 || nqb < 1 || d < 1 || blocks_per_frame < 1 || chunk_index < 1 || frames_per_chunk < 1)
     return fail(LF_ERR_INVALID, "lf_select: bad sizes");

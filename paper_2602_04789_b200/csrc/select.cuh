@@ -620,6 +620,26 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
   __shared__ double mred[8];
 
   __shared__ float s_qn[4];
+  const int current = a.f * bpf;
+  int total = current;
+  if (a.chunk > 1) total = budget_round(*a.s_i, (long long)a.chunk * current);
+  const int past_budget = total > current ? total - current : 0;
+  if (a.out_budget && w == 0 && tid == 0) {
+    a.out_budget[0] = total;
+    a.out_budget[1] = past_budget;
+    a.out_budget[2] = total < current;
+    a.out_budget[3] = 0;
+  }
+  if (past_budget == 0 && !a.out_frames && !a.out_margin && !a.out_fscores) {
+    // no past block to spend and no frame list wanted (out_frames NULL): the
+    // frame ranking cannot change any output (the mask is the current chunk,
+    // selection.py:154-155), so it is skipped
+    if (a.out_bits)
+      for (int e = tid; e < a.bits_words; e += kSelThreads)
+        a.out_bits[((size_t)h * a.nqb + r) * a.bits_words + e] = 0u;
+    if (tid == 0) a.out_count[w] = 0;
+    return;
+  }
   const float* kf = a.k_frame + (size_t)h * a.kf_head_stride;
   const float* qrow = a.q_block + ((size_t)h * a.nqb + r) * d;
   float qn = 0.f;  // |q|^2, rounded upward
@@ -633,16 +653,6 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) qn = __fadd_ru(qn, __shfl_xor_sync(0xffffffffu, qn, o));
   if (lane == 0) s_qn[tid >> 5] = qn;
-  const int current = a.f * bpf;
-  int total = current;
-  if (a.chunk > 1) total = budget_round(*a.s_i, (long long)a.chunk * current);
-  const int past_budget = total > current ? total - current : 0;
-  if (a.out_budget && w == 0 && tid == 0) {
-    a.out_budget[0] = total;
-    a.out_budget[1] = past_budget;
-    a.out_budget[2] = total < current;
-    a.out_budget[3] = 0;
-  }
   __syncthreads();
   // screening bound scale gamma |q|_2, rounded upward
   const float qscale =
@@ -678,8 +688,10 @@ __global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a
   __syncthreads();
   const int nsel = s_nsel;
   SEL_MARK(3);
-  int* of = a.out_frames + ((size_t)h * a.nqb + r) * a.frame_cap;
-  for (int e = tid; e < a.frame_cap; e += kSelThreads) of[e] = e < nsel ? fsel[e] : -1;
+  if (a.out_frames) {
+    int* of = a.out_frames + ((size_t)h * a.nqb + r) * a.frame_cap;
+    for (int e = tid; e < a.frame_cap; e += kSelThreads) of[e] = e < nsel ? fsel[e] : -1;
+  }
 
   const int C = nsel * bpf;
   double* om = a.out_margin ? a.out_margin + 2 * ((size_t)h * a.nqb + r) : nullptr;

@@ -290,10 +290,12 @@ def plan_tiles(blocks, count, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
 
 def select_plan(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: int,
                 per_frame: bool, s_i, qt: TilingSpec, kt: TilingSpec, list_blocks: int,
-                want_margin: bool = False):
+                want_margin: bool = False, want_frames: bool = True):
     """select() + plan_tiles() of one step (lf_select_plan).  Returns
     (Selections, TilePlan, margin) with margin = [H, nqb, 2] fp64 top-k margin
-    certificate (frames, blocks) or None."""
+    certificate (frames, blocks) or None.  want_frames=False: Selections.frames
+    is None and a step whose past budget is 0 skips the frame ranking (it
+    cannot change the blocks)."""
     lib = L.lib()
     H, nqb, d = q_block.shape
     nkb = k_block.shape[1]
@@ -308,7 +310,8 @@ def select_plan(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: i
         assert t.stride(2) == 1 and t.stride(1) == d, "summaries must have contiguous rows"
     blocks = torch.empty((H, nqb, cap), dtype=torch.int32, device=dev)
     count = torch.empty((H, nqb), dtype=torch.int32, device=dev)
-    frames = torch.empty((H, nqb, frame_cap), dtype=torch.int32, device=dev)
+    frames = (torch.empty((H, nqb, frame_cap), dtype=torch.int32, device=dev)
+              if want_frames else None)
     budget = torch.empty(4, dtype=torch.int32, device=dev)  # all four written by the kernel
     margin = torch.empty((H, nqb, 2), dtype=torch.float64, device=dev) if want_margin else None
     rows = plan_rows()
@@ -326,7 +329,7 @@ def select_plan(q_block, k_block, k_frame, bpf: int, chunk: int, f: int, topk: i
                                k_frame.stride(0) if P > 0 else 0, H, nqb, nkb, d, int(bpf),
                                int(chunk), int(f), int(topk), 1 if per_frame else 0,
                                s_i.data_ptr(), cap, frame_cap, blocks.data_ptr(),
-                               count.data_ptr(), frames.data_ptr(), budget.data_ptr(),
+                               count.data_ptr(), L.ptr(frames), budget.data_ptr(),
                                L.ptr(margin), qt.abi(), kt.abi(), int(list_blocks), int(seg_cap),
                                segs.data_ptr(), seg_count.data_ptr(), L.ptr(qperm),
                                L.stream_ptr()))

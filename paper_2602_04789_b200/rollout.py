@@ -34,8 +34,13 @@ from .selection import SelectionConfig, tilings
 class HsaRollout:
     def __init__(self, layout: ChunkLayout, heads: int, plan: SparsityPlan | None = None,
                  cfg: SelectionConfig | None = None, framewise: bool | None = None,
-                 out_dtype=torch.bfloat16, device=None):
+                 out_dtype=torch.bfloat16, device=None, keep_frames: bool = False):
+        """keep_frames: also return each step's retrieved past frames
+        (StepPlan.selection.frames, else None).  Nothing downstream of the
+        selection reads them, and without them a step whose past budget is 0
+        skips the frame ranking (it cannot change the mask)."""
         self.layout = layout = as_layout(layout)
+        self.keep_frames = bool(keep_frames)
         self.heads = int(heads)
         self.plan = plan
         self.cfg = cfg or SelectionConfig()
@@ -196,7 +201,7 @@ class HsaRollout:
             sel, tiles, _ = D.select_plan(q_block, self.kb_cache, self.kf_cache, self.bpf, i,
                                           lay.f, self.cfg.topk_frames,
                                           self.cfg.block_budget_mode == "per-frame", s_dev, qt,
-                                          kt, P * self.bpf)
+                                          kt, P * self.bpf, want_frames=self.keep_frames)
             qmode = D.qtile_mode(qt)
         hint = D.past_tiles_hint(s_host, i, lay.f, self.bpf, self.cfg.topk_frames, qt)
         self.last_selection = sel

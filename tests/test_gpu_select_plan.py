@@ -280,3 +280,41 @@ def test_margin_certificate_baseline_shapes(D, chunk, s_i):
                 worst = min(worst, mg[h, r, 1] / bb)
     print(f"chunk {chunk}: min margin / fp64 reordering bound = {worst:.3e}; "
           f"min frame margin {mg[..., 0].min():.3e}, min block margin {mg[..., 1].min():.3e}")
+
+
+@pytest.mark.parametrize("chunk,s_i,qmode", [(7, 6 / 7, 0), (7, 6 / 7, 2), (7, 0.5, 0),
+                                             (14, 0.8, 1), (1, 0.0, 0)])
+def test_select_plan_without_frames(D, chunk, s_i, qmode):
+    """want_frames=False (out_frames NULL): the same blocks, counts, budget and
+    tile plan as with the frame list; at a past budget of 0 (the c2 plan) the
+    frame ranking is skipped, and a forced geometry 2 still pairs (empty
+    bitsets)."""
+    H, f, n, d, topk = 2, 3, 1560, 128, 6
+    bpf = -(-n // 64)
+    qt = D.TilingSpec(f * n, n, 64)
+    kt = D.TilingSpec(chunk * f * n, n, 64)
+    P = (chunk - 1) * f
+    qb, kb, kf = _summaries(31 + chunk, H, qt.count, kt.count, P, d, False)
+    dev = torch.device("cuda")
+    tq, tk, tf = (torch.from_numpy(a).to(dev) for a in (qb, kb, kf))
+    with D.qtile_scope(qmode):
+        a, ta, _ = D.select_plan(tq, tk, tf, bpf, chunk, f, topk, False, s_i, qt, kt, P * bpf)
+        b, tb, _ = D.select_plan(tq, tk, tf, bpf, chunk, f, topk, False, s_i, qt, kt, P * bpf,
+                                 want_frames=False)
+    torch.cuda.synchronize()
+    assert b.frames is None
+    assert torch.equal(a.count, b.count) and torch.equal(a.budget[:3], b.budget[:3])
+    cnt = a.count.cpu()
+    for h in range(H):
+        for r in range(qt.count):
+            c = int(cnt[h, r])
+            assert torch.equal(a.blocks[h, r, :c], b.blocks[h, r, :c])
+    assert torch.equal(ta.seg_count, tb.seg_count)
+    sc = ta.seg_count.cpu()
+    for h in range(H):
+        for t in range(sc.shape[1]):
+            assert torch.equal(ta.segs[h, t, :sc[h, t]], tb.segs[h, t, :sc[h, t]])
+    if ta.qperm is not None:
+        assert torch.equal(ta.qperm, tb.qperm)
+    if chunk == 7 and s_i == 6 / 7:
+        assert int(a.budget[1]) == 0 and int(cnt.sum()) == 0
