@@ -925,7 +925,8 @@ static int pair_words(int list_blocks) { return (((list_blocks > 0 ? list_blocks
 
 static int pair_launch(const int32_t* blocks, const int32_t* count, int32_t heads, int32_t nqb,
                        int32_t cap, int32_t list_blocks, int32_t* qperm,
-                       const unsigned int* bits_in, void* stream) {
+                       const unsigned int* bits_in, void* stream,
+                       unsigned short* ov_scratch = nullptr) {
   if (!qperm || !blocks || !count || heads < 1 || nqb < 1 || cap < 1)
     return fail(LF_ERR_INVALID, "lf_pair_qblocks: bad args");
   const int lb = list_blocks > 0 ? list_blocks : 0;
@@ -936,7 +937,13 @@ static int pair_launch(const int32_t* blocks, const int32_t* count, int32_t head
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(pair_qblocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  PairArgs a{blocks, count, nqb, cap, lb, words, qperm, bits_in};
+  PairArgs a{blocks, count, nqb, cap, lb, words, qperm, bits_in, nullptr};
+  if (bits_in && ov_scratch) {  // overlaps over the SMs first (one CTA per query block)
+    launch_step(pair_overlap_kernel, heads * nqb, kOvThreads, 0, stream, a, ov_scratch);
+    int rc;
+    if ((rc = check_launch("pair_overlap_kernel"))) return rc;
+    a.ov_in = ov_scratch;
+  }
   launch_step(pair_qblocks_kernel, heads, kPairThreads, smem, stream, a);
   return check_launch("pair_qblocks_kernel");
 }
@@ -1010,6 +1017,14 @@ int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_s
       (size_t)heads * nqb * words * 4 <=
           (size_t)heads * plan_tile_count(q_tiling) * (seg_cap > 0 ? seg_cap : 0) * 16)
     bits = reinterpret_cast<unsigned int*>(segs);
+  // and the overlap matrix behind the bitsets, when the segment buffer holds both
+  unsigned short* ov = nullptr;
+  if (bits) {
+    const size_t off = align_up((size_t)heads * nqb * words * 4, 16);
+    if (off + (size_t)heads * nqb * nqb * 2 <=
+        (size_t)heads * plan_tile_count(q_tiling) * (seg_cap > 0 ? seg_cap : 0) * 16)
+      ov = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(segs) + off);
+  }
   if ((rc = select_launch(q_block, k_block, kb_head_stride, k_frame, kf_head_stride, heads, nqb,
                           nkb, d, blocks_per_frame, chunk_index, frames_per_chunk, topk_frames,
                           per_frame_mode, s_i_dev, cap, frame_cap, out_blocks, out_count,
@@ -1017,7 +1032,7 @@ int lf_select_plan(const float* q_block, const float* k_block, int64_t kb_head_s
                           bits ? words : 0)))
     return rc;
   if (paired && (rc = pair_launch(out_blocks, out_count, heads, nqb, cap, list_blocks, qperm,
-                                  bits, stream)))
+                                  bits, stream, ov)))
     return rc;
   return lf_plan_tiles_paired(out_blocks, out_count, heads, nqb, cap, q_tiling, k_tiling,
                               list_blocks, seg_cap, segs, seg_count, paired ? qperm : nullptr,

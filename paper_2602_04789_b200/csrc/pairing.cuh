@@ -54,7 +54,30 @@ struct PairArgs {
   int nqb, cap, list_blocks, words;
   int* qperm;         // [H][2 * ceil(nqb / 2)]
   const unsigned int* bits_in;  // optional [H][nqb][words]: the bitsets, written by the selection
+  const unsigned short* ov_in;  // optional [H][nqb][nqb]: the overlaps (pair_overlap_kernel)
 };
+
+// Pairwise overlaps of the selection bitsets, spread over the SMs: one CTA per
+// (head, query block x) writes row x of the head's overlap matrix (the single
+// per-head CTA of pair_qblocks_kernel was issue-bound on its SM doing all of
+// them).  ov[h][x][y] = min(popc(bits_x & bits_y), 2047); row x == column x.
+constexpr int kOvThreads = 128;
+__global__ void __launch_bounds__(kOvThreads) pair_overlap_kernel(PairArgs a, unsigned short* ov) {
+  __shared__ unsigned int bx[64];
+  const int n = a.nqb, W = a.words;
+  const int h = blockIdx.x / n, x = blockIdx.x - h * n;
+  pdl_wait();
+  const unsigned int* bh = a.bits_in + (size_t)h * n * W;
+  for (int w = threadIdx.x; w < W; w += kOvThreads) bx[w] = __ldg(bh + (size_t)x * W + w);
+  __syncthreads();
+  unsigned short* row = ov + ((size_t)h * n + x) * n;
+  for (int y = threadIdx.x; y < n; y += kOvThreads) {
+    const unsigned int* by = bh + (size_t)y * W;
+    int c = 0;
+    for (int w = 0; w < W; ++w) c += __popc(bx[w] & __ldg(by + w));
+    row[y] = (unsigned short)(c < 2047 ? c : 2047);  // keeps the packed proposal key positive
+  }
+}
 
 __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) {
   extern __shared__ __align__(16) unsigned int pr_smem[];
@@ -76,7 +99,14 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
   if (!a.bits_in)
     for (int i = tid; i < n * W; i += NT) bits[i] = 0u;
   int any = 0;
-  if (a.bits_in) {  // bitsets from the selection kernel: one coalesced copy
+  if (a.ov_in) {  // overlaps from pair_overlap_kernel: one coalesced copy
+    const unsigned short* src = a.ov_in + (size_t)h * n * n;
+    for (int i = tid; i < n * n; i += NT) ov[i] = __ldg(src + i);
+    for (int i = tid; i < n; i += NT) {
+      mate[i] = -1;
+      any |= __ldg(src + (size_t)i * n + i) != 0;  // own selection non-empty
+    }
+  } else if (a.bits_in) {  // bitsets from the selection kernel: one coalesced copy
     for (int i = tid; i < n; i += NT) mate[i] = -1;
     const unsigned int* src = a.bits_in + (size_t)h * n * W;
     for (int i = tid; i < n * W; i += NT) {
@@ -85,7 +115,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
       any |= v != 0u;
     }
   }
-  for (int i = tid; !a.bits_in && i < n; i += NT) {
+  for (int i = tid; !a.bits_in && !a.ov_in && i < n; i += NT) {
     mate[i] = -1;
     const int c = __ldg(a.count + (size_t)h * n + i);
     cnt[i] = c < a.cap ? c : a.cap;
@@ -96,7 +126,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
   // rows (different words: no atomic conflicts), R-strided entries per thread
   const int* lst = a.blocks + (size_t)h * n * a.cap;
   const int R = n < NT ? NT / n : 1;
-  for (int task = tid; !a.bits_in && task < n * R; task += NT) {
+  for (int task = tid; !a.bits_in && !a.ov_in && task < n * R; task += NT) {
     const int x = task % n, k = task / n, c = cnt[x];
     const int* row = lst + (size_t)x * a.cap;
 #pragma unroll 4
@@ -114,7 +144,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
     // consecutive threads on consecutive y (rows of odd word stride: conflict-free
     // reads of row y, broadcast of row x) -- every pair in flight at once instead
     // of a warp walking its rows
-    for (int pi = tid; pi < n * n; pi += NT) {
+    for (int pi = tid; !a.ov_in && pi < n * n; pi += NT) {
       const int x = pi / n, y = pi - x * n;
       if (y <= x) continue;
       const unsigned int* bx = bits + x * W;
@@ -128,22 +158,31 @@ __global__ void __launch_bounds__(kPairThreads) pair_qblocks_kernel(PairArgs a) 
 #ifdef LF_PAIR_TRACE
     tr[2] = clock64();
 #endif
-    // mutual-best rounds; a thread per proposing block scans its row of the
-    // overlap matrix, key = (overlap, nearer, lower index)
+    // mutual-best rounds; a warp per proposing block scans its row of the
+    // overlap matrix (lanes on consecutive partners, warp max), key =
+    // (overlap, nearer, lower index)
+    // A block's best partner stays its best while that partner is unpaired
+    // (availability only shrinks), so after the first round only blocks whose
+    // proposal was paired away rescan their row.
+    const int lane = tid & 31, warp = tid >> 5;
     for (int round = 0; round < n; ++round) {
-      for (int x = tid; x < n; x += NT) {
+      for (int x = warp; x < n; x += NT / 32) {
         int best = -1;
-        if (mate[x] < 0) {
+        const int cur = prop[x];
+        if (mate[x] < 0 && round > 0 && cur >= 0 && mate[cur] < 0) {
+          best = cur;
+        } else if (mate[x] < 0) {
           int key = -1;
           const unsigned short* row = ov + x * n;
-          for (int y = 0; y < n; ++y) {
+          for (int y = lane; y < n; y += 32) {
             const int dist = y > x ? y - x : x - y;
             const int kk = ((int)row[y] << 20) | ((1023 - dist) << 10) | (1023 - y);
             key = (y != x && mate[y] < 0 && kk > key) ? kk : key;
           }
+          key = __reduce_max_sync(0xffffffffu, key);
           best = key >= 0 ? 1023 - (key & 1023) : -1;
         }
-        prop[x] = best;
+        if (lane == 0) prop[x] = best;
       }
       if (tid == 0) s_new = 0;
       __syncthreads();

@@ -150,3 +150,73 @@ def test_rollout_paired_matches_blocks_geometry(lf):
     assert res[2][2] <= res[1][2], (res[1][2], res[2][2])
     print(f"issued tile FLOPs: blocks {res[1][2]:.3e}, paired {res[2][2]:.3e} "
           f"({100 * (res[2][2] / res[1][2] - 1):+.1f} %)")
+
+
+def _pair_ref(blocks, count, L):
+    """CPU restatement of pair_qblocks_kernel (pairing.cuh): overlaps, mutual-best
+    rounds (key = overlap, nearer, lower index), tiles in serial-scan order."""
+    H, n, _ = blocks.shape
+    out = np.full((H, 2 * ((n + 1) // 2)), -1, np.int32)
+    for h in range(H):
+        sets = [set(int(b) for b in blocks[h, x, :count[h, x]] if 0 <= b < L) for x in range(n)]
+        ov = [[min(len(sets[x] & sets[y]), 2047) for y in range(n)] for x in range(n)]
+        mate = [-1] * n
+        if any(sets):
+            for _ in range(n):
+                prop = [-1] * n
+                for x in range(n):
+                    if mate[x] >= 0:
+                        continue
+                    key = -1
+                    for y in range(n):
+                        if y != x and mate[y] < 0:
+                            key = max(key, (ov[x][y] << 20) | ((1023 - abs(x - y)) << 10) | (1023 - y))
+                    prop[x] = 1023 - (key & 1023) if key >= 0 else -1
+                new = 0
+                for x in range(n):
+                    y = prop[x]
+                    if y >= 0 and prop[y] == x:
+                        mate[x] = y
+                        new += x < y
+                if new == 0:
+                    break
+        tiles, ul = [], []
+        for x in range(n):
+            if mate[x] > x:
+                tiles.append((x, mate[x]))
+            elif mate[x] < 0:
+                ul.append(x)
+                if len(ul) % 2 == 0:
+                    tiles.append((ul[-2], ul[-1]))
+        if len(ul) % 2:
+            tiles.append((ul[-1], -1))
+        out[h, :2 * len(tiles)] = np.asarray(tiles, np.int32).ravel()
+    return out
+
+
+@pytest.mark.parametrize("kind", ["random", "clustered", "empty"])
+def test_pairing_matches_cpu_restatement(lf, kind):
+    """Both pairing paths (lists: lf_pair_qblocks; bitsets + the overlap kernel:
+    lf_select_plan) equal a CPU restatement of the mutual-best rounds."""
+    from paper_2602_04789_b200 import device as D
+    rng = np.random.default_rng({"random": 11, "clustered": 12, "empty": 13}[kind])
+    H, nqb, cap, L = 2, 75, 150, 450
+    blocks = np.full((H, nqb, cap), -1, np.int32)
+    count = np.zeros((H, nqb), np.int32)
+    if kind != "empty":
+        for h in range(H):
+            for r in range(nqb):
+                if kind == "random":
+                    c = int(rng.integers(0, cap))
+                    sel = rng.choice(L, c, replace=False)
+                else:  # groups of blocks share most of a frame range: long proposal chains
+                    base = (r // 5) * 25 % L
+                    pool = np.arange(base, base + 90) % L
+                    c = int(rng.integers(40, 90))
+                    sel = rng.choice(pool, c, replace=False)
+                blocks[h, r, :c] = np.sort(sel)
+                count[h, r] = c
+    dev = torch.device("cuda")
+    tb, tc = torch.from_numpy(blocks).to(dev), torch.from_numpy(count).to(dev)
+    got = D.pair_qblocks(tb, tc, L).cpu().numpy()
+    np.testing.assert_array_equal(got, _pair_ref(blocks, count, L))
