@@ -909,9 +909,9 @@ def run_ours(args, c):
     # pool(Q+K), pool(k_frame), select, plan_tiles, attention; chunk 1 has no past stages
     # rollout flow per chunk: commit (2 pool launches) + T x (pool Q, select,
     # plan tiles, attention); chunk 1 has no past (no commit, no tile plan)
-    # (+ the pairing kernel per step under query-tile geometry 2)
+    # (+ the two pairing kernels per step under query-tile geometry 2)
     paired = int(getattr(pl, "qmode", 0) or 0) == 2
-    launches_per_chunk = T * ((4 if P > 0 else 3) + (1 if paired else 0)) + (2 if i > 1 else 0)
+    launches_per_chunk = T * ((4 if P > 0 else 3) + (2 if paired else 0)) + (2 if i > 1 else 0)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
