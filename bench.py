@@ -593,6 +593,31 @@ def run_ours(args, c):
         timeline_dump(run_chunk, os.environ["LF_BENCH_TIMELINE"])
         timeline_dump(chunk_flow, os.environ["LF_BENCH_TIMELINE"] + ".eager.csv")
     value = flops_r_step / (ms_chunk_r * 1e-3) / 1e12
+    if os.environ.get("LF_BENCH_PROBE") and rank == 0:
+        # profiling aid: the rollout's attention calls alone (plans prepared once),
+        # each in its own graph, replayed back to back -- against the stage timing
+        pls = [ro.prepare(Q[s], i, s_i=s_dev, s_host=s_host) for s in range(T)]
+        gA = []
+        for s in range(T):
+            ro.attend(pls[s], out=r_out[s])
+        torch.cuda.synchronize()
+        for s in range(T):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                ro.attend(pls[s], out=r_out[s])
+            gA.append(g)
+        for variant in ("rotate", "same"):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for s in range(T):
+                gA[s].replay()
+            a_.record()
+            for _ in range(10):
+                for s in range(T):
+                    gA[s if variant == "rotate" else 0].replay()
+            b_.record()
+            torch.cuda.synchronize()
+            sys.stderr.write(f"probe: rollout attention alone ({variant}) "
+                             f"{a_.elapsed_time(b_) / (10 * T) * 1e3:.1f} us/call\n")
     errs += int(ro.err.item())
 
     # ---- kernel-level timing for the roofline: the same kernels on the same
@@ -651,6 +676,8 @@ def run_ours(args, c):
         torch.cuda.synchronize()
         stage[name].append(ea.elapsed_time(eb) / (reps * T))
     attn_ms = statistics.mean(stage["attn"])
+    if os.environ.get("LF_BENCH_PROBE") and rank == 0:
+        sys.stderr.write(f"probe: stage attention (stateless inputs) {attn_ms * 1e3:.1f} us/call\n")
     pool_ms = statistics.mean(stage["pool"])
     sel_ms = statistics.mean(stage["select"])
     peaks = {}
