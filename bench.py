@@ -479,33 +479,21 @@ def run_ours(args, c):
     # Step order (LF_BENCH_FLOW).  serial (the headline): each call's pool q ->
     # select -> plan -> attention in order on one stream, call after call -- what
     # a denoiser allows, whose query of step s+1 depends on the output of step s.
-    # A/B only: overlap (the selection half of step s+1 enqueued on a side stream
-    # while step s attends, round 1-2's headline), prio (overlap with the
-    # attention stream at high priority), prio2 (prio, steps alternating between
-    # two side streams); these let step s+1's selection run beside step s's
-    # attention, which a real denoiser cannot (profiles/r02/flow_ab.txt)
+    # overlap (A/B only, rounds 1-2's headline): the selection half of step s+1
+    # enqueued on a side stream while step s attends, which a real denoiser
+    # cannot do (profiles/r02/flow_ab.txt; two stream-priority variants measured
+    # there were dropped)
     flow = os.environ.get("LF_BENCH_FLOW", "serial")
-    sides = [torch.cuda.Stream(priority=0) for _ in range(2 if flow == "prio2" else 1)]
-    side = sides[0]
+    if flow not in ("serial", "overlap"):
+        raise SystemExit(f"LF_BENCH_FLOW={flow}: serial | overlap")
+    side = torch.cuda.Stream()
     comm = torch.cuda.Stream()
-    hi = torch.cuda.Stream(priority=-1) if flow in ("prio", "prio2") else None
     ev_prep = [torch.cuda.Event() for _ in range(T)]
 
     def chunk_flow():
-        if hi is not None:
-            hi.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(hi):
-                plans = chunk_flow_on()
-            torch.cuda.current_stream().wait_stream(hi)
-            return plans
-        return chunk_flow_on()
-
-    def chunk_flow_on():
         main = torch.cuda.current_stream()
         if i > 1:
             ro.commit(None, None, i - 1, overwrite=True)
-        for sd in sides:
-            sd.wait_stream(main)
         plans = [None] * T
         if flow == "serial":
             for s in range(T):
@@ -516,12 +504,12 @@ def run_ours(args, c):
             if mode == "headshard":
                 main.wait_stream(comm)
             return plans
+        side.wait_stream(main)
 
         def prep(s):
-            sd = sides[s % len(sides)]
-            with torch.cuda.stream(sd):
+            with torch.cuda.stream(side):
                 plans[s] = ro.prepare(Q[s], i, s_i=s_dev, s_host=s_host)
-                ev_prep[s].record(sd)
+                ev_prep[s].record(side)
         prep(0)
         for s in range(T):
             if s + 1 < T:
@@ -530,8 +518,7 @@ def run_ours(args, c):
             ro.attend(plans[s], out=r_out[s])
             if mode == "headshard":  # all-gather of call s overlaps the compute of s+1
                 gather_heads_overlapped(r_out[s], shard, full[s], comm)
-        for sd in sides:
-            main.wait_stream(sd)
+        main.wait_stream(side)
         if mode == "headshard":
             main.wait_stream(comm)
         return plans
