@@ -173,6 +173,12 @@ int sm_count() {
   return v;
 }
 
+// CTAs per SM the frame-split pooling launches aim for (query pooling of a
+// rollout step, chunk commits)
+#ifndef LF_POOL_WANT
+#define LF_POOL_WANT 2
+#endif
+
 // K1 launch (pool.cuh pool_frames_tma_kernel): contiguous bf16 rows, d 64/128,
 // blocks <= 64 rows.  LF_OPT_POOL_CFG picks (consumer groups x ring stages).
 void launch_frame_pool_tma(const FramePoolArgs& fa, int d, int smem, int grid, void* stream) {
@@ -681,7 +687,7 @@ int lf_pool_blocks(const lf_mat* x, lf_tiling tiling, int32_t max_blocks, float*
       fa.per_period = per;
       fa.q_frames = frames;
       fa.k_split = 1;
-      const int want = 2 * sm_count();
+      const int want = LF_POOL_WANT * sm_count();
       int split = (want + x->heads * frames - 1) / (x->heads * frames);
       split = split < 1 ? 1 : (split > per ? per : split);
       fa.q_split = split;
@@ -824,7 +830,7 @@ int lf_pool_chunk_k(const lf_mat* k, lf_tiling k_tiling, int32_t blocks_per_fram
   // a chunk is only H*f frames (36 CTAs at 12 heads): split the frames into block
   // ranges so that the grid covers the SMs, then pool the frame summaries from
   // the written block means in a second, tiny launch
-  const int want = 2 * sm_count();
+  const int want = LF_POOL_WANT * sm_count();
   int split = (want + k->heads * fa.k_frames - 1) / (k->heads * fa.k_frames);
   split = split < 1 ? 1 : (split > per ? per : split);
   fa.k_split = split;
