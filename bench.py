@@ -395,7 +395,10 @@ def run_ours(args, c):
     Q = [gen(s, lq, h0) for s in range(T)]
     K = [gen(s + 100, lk, h0) for s in range(T)]
     V = [gen(s + 200, lk, h0) for s in range(T)]
-    pipes = [lf.HsaPipeline(lay, h_local, i, cfg, framewise=True, out_dtype=torch.bfloat16)
+    # the per-call contract returns the output (hsa_attention's mask comes from the
+    # blocks): no frame lists, so a call with past budget 0 skips the frame ranking
+    pipes = [lf.HsaPipeline(lay, h_local, i, cfg, framewise=True, out_dtype=torch.bfloat16,
+                            keep_frames=False)
              for _ in range(T)]
     outs = [p.bind(Q[s], K[s], V[s], s_dev, s_host=s_host) for s, p in enumerate(pipes)]
     full = [torch.empty((H, lq, d), dtype=torch.bfloat16, device=dev) for _ in range(T)] \

@@ -282,6 +282,10 @@ typedef struct {
   int32_t* err_flag;        /* optional                                       */
   int32_t attn_kernel;      /* LF_KERNEL_AUTO / _TILE / _PAIR                 */
   double s_i_host;          /* host copy of s_i for LF_KERNEL_AUTO (NaN: unknown) */
+  int32_t skip_frames;      /* 1: the retrieved-frame lists are not wanted (the
+                               frames view is left unwritten; a call whose past
+                               budget is 0 skips the frame ranking, which cannot
+                               change the mask); 0: written, as before       */
 } lf_hsa_args;
 
 /* The workspace holds every intermediate of the call (summaries, selections,

@@ -63,7 +63,8 @@ class LfHsaArgs(ctypes.Structure):
                 ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
                 ("out_row_stride", ctypes.c_int64), ("out_head_stride", ctypes.c_int64),
                 ("lse", ctypes.c_void_p), ("err_flag", ctypes.c_void_p),
-                ("attn_kernel", ctypes.c_int32), ("s_i_host", ctypes.c_double)]
+                ("attn_kernel", ctypes.c_int32), ("s_i_host", ctypes.c_double),
+                ("skip_frames", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p

@@ -1191,7 +1191,8 @@ int lf_hsa_forward(const lf_hsa_args* a, void* workspace, size_t workspace_bytes
   if ((rc = lf_select_plan(w.q_block, w.k_block, (int64_t)g.nkb * g.d, w.k_frame,
                            (int64_t)g.P * g.d, g.H, g.nqb, g.nkb, g.d, g.bpf, a->chunk_index,
                            a->f, a->topk_frames, a->per_frame_mode, a->s_i_dev, g.cap,
-                           g.frame_cap, w.blocks, w.count, w.frames, w.budget, nullptr, g.qt,
+                           g.frame_cap, w.blocks, w.count, a->skip_frames ? nullptr : w.frames,
+                           w.budget, nullptr, g.qt,
                            g.kt, g.list_blocks, g.seg_cap, reinterpret_cast<int32_t*>(w.segs),
                            w.seg_count, w.qperm, stream)))
     return rc;

@@ -23,8 +23,12 @@ from .selection import SelectionConfig, mask_from_lists, tilings
 class HsaPipeline:
     def __init__(self, layout: ChunkLayout, heads: int, chunk_index: int,
                  cfg: SelectionConfig | None = None, framewise: bool | None = None,
-                 out_dtype=torch.bfloat16, device=None):
+                 out_dtype=torch.bfloat16, device=None, keep_frames: bool = True):
+        """keep_frames=False: selections() returns no frame lists (None), and a
+        call whose past budget is 0 skips the frame ranking (it cannot change
+        the mask) -- what the bench's stateless leg runs."""
         self.layout = layout = as_layout(layout)
+        self.keep_frames = bool(keep_frames)
         self.heads = int(heads)
         self.chunk = int(chunk_index)
         self.cfg = cfg or SelectionConfig()
@@ -66,6 +70,7 @@ class HsaPipeline:
         a.err_flag = self.err.data_ptr()
         a.attn_kernel = self.attn_kernel
         a.s_i_host = float("nan") if self._s_host is None else float(self._s_host)
+        a.skip_frames = 0 if self.keep_frames else 1
         return a
 
     def bind(self, q, k, v, s_i, out=None, s_host=None):
@@ -152,7 +157,8 @@ class HsaPipeline:
         H, nqb = self.heads, self.qt.count
         blocks = self._read(ptrs[3].value, H * nqb * cap, torch.int32).view(H, nqb, cap)
         count = self._read(ptrs[4].value, H * nqb, torch.int32).view(H, nqb)
-        frames = self._read(ptrs[5].value, H * nqb * fcap, torch.int32).view(H, nqb, fcap)
+        frames = (self._read(ptrs[5].value, H * nqb * fcap, torch.int32).view(H, nqb, fcap)
+                  if self.keep_frames else None)
         budget = self._read(ptrs[6].value, 4, torch.int32)
         return blocks, count, frames, budget
 

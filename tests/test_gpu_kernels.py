@@ -171,3 +171,34 @@ def test_rollouts_have_independent_attention_scratch(lf):
     assert a.scratch.data_ptr() != b.scratch.data_ptr()
     assert a.scratch.numel() == L.lib().lf_attention_scratch_bytes(2, L.tiling(4680, 1560, 64), 128)
     assert int(a.scratch.sum()) == 0
+
+
+@pytest.mark.parametrize("i,s_i", [(7, 6 / 7), (7, 0.5)])
+def test_pipeline_without_frames_is_bit_identical(lf, i, s_i):
+    """HsaPipeline(keep_frames=False) (lf_hsa_args.skip_frames): the same output
+    bits, blocks and counts as with the frame lists; at a past budget of 0 (the
+    c2 plan) the frame ranking is skipped."""
+    H, f, n, d = 2, 3, 1560, 128
+    lay = lf.ChunkLayout(f=f, n=n, b_q=64, b_kv=64, d=d, N=7)
+    cfg = lf.SelectionConfig(topk_frames=6)
+    g = torch.Generator(device="cuda").manual_seed(100 + i)
+    q = torch.randn((H, f * n, d), device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn((H, i * f * n, d), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((H, i * f * n, d), device="cuda", generator=g).to(torch.bfloat16)
+    s_dev = torch.tensor([s_i], dtype=torch.float64, device="cuda")
+    outs, sels = [], []
+    for keep in (True, False):
+        pipe = lf.HsaPipeline(lay, H, i, cfg, framewise=True, keep_frames=keep)
+        outs.append(pipe(q, k, v, s_dev, s_host=s_i).clone())
+        sels.append(pipe.selections())
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    (b0, c0, f0, g0), (b1, c1, f1, g1) = sels
+    assert f0 is not None and f1 is None
+    assert torch.equal(c0, c1) and torch.equal(g0[:3], g1[:3])
+    for h in range(H):
+        for r in range(c0.shape[1]):
+            m = int(c0[h, r])
+            assert torch.equal(b0[h, r, :m], b1[h, r, :m])
+    if s_i == 6 / 7:
+        assert int(g0[1]) == 0
