@@ -630,8 +630,10 @@ def run_ours(args, c):
         def run_sel(s=s, st=st):
             qb, kb, kf = st["views"]
             with D.qtile_scope(qmode):
+                # as the per-call pipeline runs it (no frame lists: skip_frames)
                 _, st["tiles"], _ = D.select_plan(qb, kb, kf, bpf, i, f, c["topk"],
-                                                  c["mode"] == "per-frame", s_dev, qt, kt, P * bpf)
+                                                  c["mode"] == "per-frame", s_dev, qt, kt, P * bpf,
+                                                  want_frames=False)
 
         def run_attn(s=s, st=st):
             with D.qtile_scope(qmode):
