@@ -592,7 +592,10 @@ __device__ __noinline__ double list_margin(const double* x, const unsigned char*
   return m;
 }
 
-__global__ void __launch_bounds__(kSelThreads, 7) select_screen_kernel(SelArgs a) {
+#ifndef LF_SEL_MINB
+#define LF_SEL_MINB 7  // resident CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(kSelThreads, LF_SEL_MINB) select_screen_kernel(SelArgs a) {
   extern __shared__ __align__(16) unsigned char sel_smem[];
   const int tid = threadIdx.x, lane = tid & 31;
   pdl_wait();
