@@ -271,7 +271,9 @@ __global__ void __launch_bounds__(320, 1)
     const uint64_t qd0 = smem_desc_sw128(smem_u32(sQ), 16, 1024);
     const uint64_t kd0 = smem_desc_sw128(smem_u32(sK), 16, 1024);
     const uint64_t vd0 = smem_desc_sw128(smem_u32(sV), C::BN * 128, 1024);
-    uint32_t kit = 0, nq = 0, np[2] = {0, 0}, noe = 0;
+    // per-set state in scalars (x-indexed arrays went to local memory on the
+    // MMA warp's issue path)
+    uint32_t kit = 0, nq = 0, np0 = 0, np1 = 0, noe = 0;
     for (int it = 0;; ++it) {
       const int w = take_item(it);
       if (w < 0) break;
@@ -283,12 +285,14 @@ __global__ void __launch_bounds__(320, 1)
       const uint64_t qd = qd0 + ((uint32_t)(qb * C::Q_BYTES) >> 4);
       if (lane == 0 && nq < 16) LF_T7(1536 + nq * 8 + 1, clk64());
       ++nq;
-      int pend[2] = {-1, -1};
-      uint32_t pend_kit[2] = {0, 0};
-      bool first_pv[2] = {true, true}, waited_o = false;
+      int pend0 = -1, pend1 = -1;
+      uint32_t pk0 = 0, pk1 = 0;
+      bool fpv0 = true, fpv1 = true, waited_o = false;
       int k = 0;
       auto issue_pv = [&](int x) {
-        const uint32_t t = pend_kit[x];
+        const uint32_t t = x ? pk1 : pk0;
+        const uint32_t npx = x ? np1 : np0;
+        const bool fpv = x ? fpv1 : fpv0;
         const int vs = t % C::VST;
         if (lane == 0 && t < 120) LF_T7(1024 + t * 4 + 1, clk64());
         if (!waited_o) {  // O_0 / O_1 are free once the previous epilogue read them
@@ -300,21 +304,27 @@ __global__ void __launch_bounds__(320, 1)
         const uint64_t vd = vd0 + ((uint32_t)(vs * C::KV_BYTES) >> 4);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          mbar_wait(p_full + 2 * x + hh, np[x] & 1);
+          mbar_wait(p_full + 2 * x + hh, npx & 1);
           tc_fence_after();
 #pragma unroll
           for (int kq = 0; kq < C::BN / 32; ++kq) {
             const int kk = hh * (C::BN / 32) + kq;
             tc_mma_ts_elect(tmem + C::COL_O + x * 128, tmem + C::COL_S + x * 128 + kk * 8,
                             vd + ((kk * 16 * 128) >> 4), IDESC_PV,
-                            (!first_pv[x] || kk > 0) ? 1u : 0u);
+                            (!fpv || kk > 0) ? 1u : 0u);
           }
         }
-        ++np[x];
+        if (x) {
+          ++np1;
+          fpv1 = false;
+          pend1 = -1;
+        } else {
+          ++np0;
+          fpv0 = false;
+          pend0 = -1;
+        }
         if (lane == 0 && t < 120) LF_T7(1024 + t * 4 + 2, clk64());
         tc_commit_elect(v_empty + vs);
-        first_pv[x] = false;
-        pend[x] = -1;
       };
       TileSegs nx0, nx1;  // the next two entries, loaded ahead (their latency off the loop)
       if (cx.j0 < cx.j1) nx0 = tile_segs(p, cx.segs, cx.nseg, cx.Tp, cx.j0);
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(320, 1)
         if (!((uint32_t)(ts.m0 | ts.m1) & cx.qm)) continue;
         const int x = k & 1;
         const int ks = kit % C::KST;
-        if (pend[x] >= 0) issue_pv(x);  // P_x of its previous tile still sits in S_x
+        if ((x ? pend1 : pend0) >= 0) issue_pv(x);  // P_x of its previous tile still sits in S_x
         if (lane == 0 && kit < 120) LF_T7(1024 + kit * 4 + 3, clk64());
         mbar_wait(k_full + ks, (kit / C::KST) & 1);
         if (lane == 0 && kit < 120) LF_T7(3072 + kit, clk64());
@@ -341,19 +351,24 @@ __global__ void __launch_bounds__(320, 1)
         tc_commit_elect(s_full + x);
         tc_commit_elect(k_empty + ks);
         if (lane == 0 && kit < 120) LF_T7(1024 + kit * 4, clk64());
-        pend[x] = 1;
-        pend_kit[x] = kit;
+        if (x) {
+          pend1 = 1;
+          pk1 = kit;
+        } else {
+          pend0 = 1;
+          pk0 = kit;
+        }
         ++kit;
         ++k;
       }
       // drain in issue order: the older pending tile first
-      if (pend[0] >= 0 && pend[1] >= 0) {
-        const int first = pend_kit[0] < pend_kit[1] ? 0 : 1;
+      if (pend0 >= 0 && pend1 >= 0) {
+        const int first = pk0 < pk1 ? 0 : 1;
         issue_pv(first);
         issue_pv(first ^ 1);
       } else {
-        if (pend[0] >= 0) issue_pv(0);
-        if (pend[1] >= 0) issue_pv(1);
+        if (pend0 >= 0) issue_pv(0);
+        if (pend1 >= 0) issue_pv(1);
       }
       tc_commit_elect(qempty(qb));
       if (k > 0) tc_commit_elect(o_full);
