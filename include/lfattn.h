@@ -57,7 +57,8 @@ typedef struct {
   int64_t head_stride;
 } lf_mat;
 
-/* Library identity. */
+/* Library identity.  101: lf_hsa_args gained skip_frames (callers built
+ * against 100 must be rebuilt); lf_select_plan accepts out_frames = NULL. */
 int lf_version(void);
 const char* lf_strerror(int status);
 const char* lf_last_error(void);

@@ -618,7 +618,7 @@ HsaWs carve(const HsaGeom& g, void* base) {
 // ===========================================================================
 extern "C" {
 
-int lf_version(void) { return 100; }
+int lf_version(void) { return 101; }  // 101: lf_hsa_args.skip_frames, lf_select_plan out_frames may be NULL
 
 int lf_plan_tile_rows(void) { return plan_rows(); }
 void lf_set_qtile_mode(int32_t mode) {

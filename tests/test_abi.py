@@ -24,7 +24,7 @@ def test_library_loads_and_exports_header_symbols():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.EXPORTS)
-    assert lib.lf_version() == 100
+    assert lib.lf_version() == 101
     assert lib.lf_strerror(4) == b"query-block row has no active key blocks"
 
 

@@ -41,7 +41,7 @@ def lf():
 def test_library_is_loaded(lf):
     from paper_2602_04789_b200 import _lib
     lib = _lib.lib()
-    assert lib.lf_version() == 100
+    assert lib.lf_version() == 101
 
 
 def test_mean_pool_bit_exact(lf):
